@@ -1,0 +1,434 @@
+"""Benchmark: distributed PINN training throughput (collocation points / s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" is one training epoch of the 2D cylinder-wake-shaped strong-scaling
+config (BASELINE.json configs[2]): N_pde = 500,000 global
+collocation points, N_obs = 10,000, 1,000 ghost points per interface,
+[3, 64x4, 3] tanh experts, decomposition_for_procs(N) subdomains, one expert
+per GPU.  N=1 runs on one GPU; N>1 is launched by torchrun (one process per
+GPU, NCCL point-to-point ghost exchange).  value = N_pde * K / (max over ranks
+of the device time of K epochs).
+
+`--impl reference` times the reference's own CPU implementation (flowrec,
+installed under baseline/_ref) on this host's cores on a bounded sample of the
+same workload, on rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "collocation pts/sec (train iters/s) at 1/2/4/8 B200; strong-scaling eff; vs CPU ref"
+UNIT = "colloc_pts/s"
+N_PDE = 500_000
+ARCH = dict(hidden_layers=4, width=64, activation="tanh")
+
+
+def flops_per_point(S=6, L=4, W=64, d_in=3, n_out=3):
+    """Algorithmic FLOPs of one collocation point's fwd+bwd."""
+    return 6 * S * (L - 1) * W * W + 6 * d_in * W + 6 * S * W * n_out + 45 * L * W
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """Samples nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measure_fp32_peak(torch, X):
+    """Measured FP32 FFMA throughput (TFLOP/s) of this GPU: the SIMT roofline."""
+    grid = torch.cuda.get_device_properties(0).multi_processor_count * 8
+    out = torch.empty(grid * 256, dtype=torch.float32, device="cuda")
+    iters = 4000
+    X.call("fr_bench_ffma", grid, 50, 0, X.ptr(out), X.stream_ptr())
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        X.call("fr_bench_ffma", grid, iters, 0, X.ptr(out), X.stream_ptr())
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        best = max(best, grid * 256.0 * iters * 1024.0 / t / 1e12)
+    return best
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2602_15883_b200 import _lib as X
+    from paper_2602_15883_b200.config import cylinder2d_problem
+    from paper_2602_15883_b200.runtime import TrainConfig, build_plan
+    from paper_2602_15883_b200.runtime.driver import DistributedTrainer, LocalTrainer
+
+    world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pb = cylinder2d_problem(n_procs=world, n_pde=args.n_pde, **ARCH)
+    total_epochs = args.warmup + args.steps + args.e2e_steps + 2
+    tc = TrainConfig(epochs=total_epochs, batch_size=25000, learning_rate=1e-3, weights=pb.weights,
+                     anchor=pb.anchor, lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0)
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
+    if world == 1:
+        trainer = LocalTrainer(plan, dtype=args.dtype, epochs=total_epochs)
+        worker = trainer.workers[0]
+
+        def run_epochs(e0, k):
+            trainer.run(k, start=e0, use_graphs=True, record_times=False)
+    else:
+        trainer = DistributedTrainer(plan, dtype=args.dtype, epochs=total_epochs)
+        worker = trainer.worker
+
+        def run_epochs(e0, k):
+            for e in range(e0, e0 + k):
+                trainer.epoch(e)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # L2 flush buffer (> 126 MB L2), written between timed epochs, outside the events
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    e = 0
+    run_epochs(e, args.warmup)  # first epoch eager + graph capture happen here
+    e += args.warmup
+    barrier()
+    X.launch_count = 0
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            run_epochs(e, 1)
+            b.record()
+            e += 1
+            times.append((a, b))
+        barrier()
+    t_rank = sum(a.elapsed_time(b) for a, b in times) * 1e-3
+    launches_host = X.launch_count
+    t_max = t_rank
+    if dist is not None:
+        tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    worker.check_flags()
+
+    # launches per epoch: count library launches while capturing / enqueuing one epoch
+    if world == 1:
+        lp = _launches_per_epoch(trainer, X)
+    else:
+        lp = None
+
+    # ---- e2e: host pinned inputs copied in + loss row copied out every step ----
+    obj = worker.objective
+    dev_bufs = [obj.col_pts, obj.obs_pts, obj.obs_vel] + [g["pts"] for g in obj.ghost.values()]
+    host_bufs = [b.cpu().pin_memory() for b in dev_bufs]
+    h2d = sum(b.numel() * b.element_size() for b in host_bufs)
+    row_host = torch.empty(7, dtype=torch.float64).pin_memory()
+    barrier()
+    ev = []
+    for _ in range(args.e2e_steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for d, h in zip(dev_bufs, host_bufs):
+            d.copy_(h, non_blocking=True)
+        run_epochs(e, 1)
+        row_host.copy_(worker.history_d[e], non_blocking=True)
+        b.record()
+        e += 1
+        ev.append((a, b))
+    barrier()
+    t_e2e = sum(a.elapsed_time(b) for a, b in ev) * 1e-3
+    if dist is not None:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+
+    # ---- dominant kernel: the fused PDE jet-MLP fwd+bwd, timed alone ----
+    pde = _time_pde_kernel(torch, X, worker)
+    peak = measure_fp32_peak(torch, X) if rank == 0 else None
+    if dist is not None:
+        dist.barrier()
+
+    if rank == 0:
+        n_loc = obj.n_colloc
+        fpp = flops_per_point()
+        achieved = fpp * n_loc / pde["ms"] * 1e-9  # TFLOP/s
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC,
+            "value": args.n_pde * args.steps / t_max,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps * 1e3,
+            "iters_per_s": args.steps / t_max,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32" if args.dtype == "float32" else "f64",
+            "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
+            "config": {
+                "workload": f"2D cylinder-wake strong-scaling, P={world} "
+                            f"(decomposition_for_procs), N_pde={args.n_pde}, N_obs={pb.budget.n_obs}, "
+                            f"N_ghost/interface={pb.budget.n_ghost_per_interface}, [3,64x4,3] tanh",
+                "decomposition": [list(pb.subdomains[0].spatial_counts), pb.subdomains[0].time_splits],
+                "colloc_per_rank": n_loc,
+                "l2": "flushed (256 MB write) between timed epochs, outside the events",
+            },
+            "e2e": {"value": args.n_pde * args.e2e_steps / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 56},
+            "gpu_launches": (lp * args.steps) if lp is not None else None,
+            "launches_per_step": lp,
+            "roofline": {
+                "bound": "compute", "pipe": "fp32-simt (FFMA)",
+                "kernel": "jetmlp_kernel<float,tanh,PDE,unsteady2d,64> (fr_pde_fwd_bwd)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None,
+                "peak_source": "measured FP32 FFMA probe (fr_bench_ffma) on this GPU",
+                "flops_per_point": fpp, "points_per_launch": n_loc,
+                "kernel_ms": pde["ms"], "kernel_share_of_step": pde["ms"] / (t_rank / args.steps * 1e3),
+                "traffic": None,
+            },
+            "clocks": clk,
+            "host_launches_timed": launches_host,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _launches_per_epoch(trainer, X):
+    import torch
+
+    before = X.launch_count
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        trainer._enqueue(True)
+    n = X.launch_count - before
+    del g
+    return n
+
+
+def _time_pde_kernel(torch, X, worker, reps=10):
+    obj = worker.objective
+    seg = [s for s in obj.segments if s[1] == X.MODE_PDE][0]
+    _, _, n, row, _ = seg
+    gp = obj.gpart.data_ptr() + 8 * row * worker.plan.info.np_pad
+    lp = obj.lpart.data_ptr() + 16 * row
+
+    def launch():
+        X.call("fr_pde_fwd_bwd", worker.plan.h, X.ptr(worker.kp), X.ptr(obj.col_pts), n,
+               obj.weights.pde / obj.n_colloc, gp, lp, X.ptr(obj.scratch), X.stream_ptr())
+
+    launch()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        launch()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    return {"ms": float(np.median(ms)), "n": n}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm
+# ---------------------------------------------------------------------------
+
+
+def _reference_module():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "flowrec")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import flowrec  # noqa: F401
+
+        return "reference"
+    return "port"
+
+
+def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
+    """Time the reference's LocalObjective.epoch + adam_step on a sample of the
+    P=1 workload (all obs, n_sample collocation points), all host cores."""
+    from threadpoolctl import threadpool_limits
+
+    kind = _reference_module()
+    cores = os.cpu_count()
+    from paper_2602_15883_b200.config import cylinder2d_problem
+
+    pb = cylinder2d_problem(n_procs=1, n_pde=args.n_pde, **ARCH)
+    ds = pb.datasets[0]
+    sample = ds.colloc_points[:n_sample]
+    t_epochs = []
+    with threadpool_limits(limits=cores):
+        if kind == "reference":
+            from flowrec.decomposition import RankDatasets
+            from flowrec.network import ExpertConfig, init_params
+            from flowrec.physics import FlowRegime, LossWeights
+            from flowrec.runtime import AdamState, LocalObjective, adam_step
+
+            regime = FlowRegime("unsteady2d", 100.0)
+            cfg = ExpertConfig.for_regime(regime, 4, 64, "tanh")
+            w = LossWeights(10.0, 5.0, 1.0, 1.0, 1.0)
+            obj = LocalObjective(cfg, regime, RankDatasets(ds.obs_points, ds.obs_velocity, sample, ()), w, 25000)
+            params = init_params(cfg, 0)
+            st = AdamState.zeros(cfg.n_params)
+            rng = np.random.default_rng(0)
+            t_end = time.perf_counter() + budget_s
+            while time.perf_counter() < t_end or not t_epochs:
+                t0 = time.perf_counter()
+                _, g, _ = obj.epoch(params, rng)
+                adam_step(params.flat, g, st, 1e-3)
+                t_epochs.append(time.perf_counter() - t0)
+        else:
+            from oracle import flowrec_oracle as O
+            from paper_2602_15883_b200.network import init_params
+
+            flat = init_params(pb.expert_config, 0).flat.copy()
+            m, v = np.zeros_like(flat), np.zeros_like(flat)
+            data = dict(obs_pts=ds.obs_points, obs_vel=ds.obs_velocity, colloc=sample, ghosts=[])
+            wd = dict(obs=10.0, pde=5.0, ghost_u=1.0, ghost_p_space=1.0, ghost_p_time=1.0, velocity=None)
+            t_end = time.perf_counter() + budget_s
+            step = 0
+            while time.perf_counter() < t_end or not t_epochs:
+                t0 = time.perf_counter()
+                _, g, _ = O.local_epoch(flat, pb.expert_config.arch, "tanh", "unsteady2d", 100.0, data, wd)
+                step, _ = O.adam_update(flat, g, m, v, step, 1e-3)
+                t_epochs.append(time.perf_counter() - t0)
+    t = float(np.median(t_epochs))
+    return {"value": n_sample / t, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"P=1 epoch (LocalObjective.epoch + adam_step) on {n_sample} of {args.n_pde} "
+                      f"collocation points + all {ds.n_obs} observations, {len(t_epochs)} epochs, "
+                      f"median {t:.3f} s/epoch, BLAS threads={cores}",
+            "s_per_epoch_sample": t}
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(args, budget_s=0.0)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(args, budget_s=0.0))
+    v = float(np.median([x["value"] for x in vals]))
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": args.n_pde / v * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
+            "config": {"workload": f"2D cylinder-wake strong-scaling, P=1 epoch sample of N_pde={args.n_pde}, "
+                                   "[3,64x4,3] tanh, reference CPU implementation"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--n-pde", type=int, default=N_PDE)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up epochs", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

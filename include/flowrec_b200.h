@@ -1,0 +1,153 @@
+/* C ABI of the B200 jet-MLP training engine (libflowrec_b200.so).
+ *
+ * This is the drop-in boundary for the reference's training hot path
+ * (arXiv 2602.15883, package `flowrec`).  Every entry point is asynchronous on
+ * the caller's CUDA stream, takes caller-owned device buffers (plain pointers
+ * and sizes), performs no allocation (so every call is CUDA-graph capturable)
+ * and returns 0 on success or a non-zero status with a message available from
+ * fr_last_error().
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/flowrec):
+ *   fr_plan_create        autodiff/builders.py:14-21,67-100 (_validate_arch, tape build)
+ *                         + tape.py:298-326 (per-bind shape checks, now done once)
+ *   fr_prepare_params     tape.py:314-326 (Tape.bind_params: params bound by reference)
+ *   fr_pde_fwd_bwd        builders.py:85-100 build_pde_tape + tape.py:329-371 fwd/bwd
+ *   fr_mse_fwd_bwd        builders.py:103-141 build_mse_tape + tape.py:329-371
+ *   fr_value_fwd          builders.py:67-73 build_value_tape; network.py:142-156 predict
+ *   fr_jet_fwd            builders.py:76-82,192-203 build_jet_tape/forward_jet;
+ *                         network.py:162-177 predict_jet
+ *   fr_reduce_grad        tape.py:365-371 (adjoint scatter into the flat grad, W0,b0,...)
+ *   fr_reduce_loss        objective.py:46-64 (_MiniBatched.run scalar sums)
+ *   fr_adam_step          runtime/optim.py:20-49 (clip_by_global_norm + adam_step),
+ *                         objective.py:183-198 (LossParts, compose_loss, finiteness),
+ *                         worker.py:231-244 (run_epoch history row)
+ *   fr_pack_ghost         runtime/worker.py:24-46,170-198 (anchor_normalize, messages)
+ *   fr_jet_act_forward    _kernels/__init__.py:57-60 jet_act_forward  (_cyjet.pyx:11-34)
+ *   fr_jet_act_backward   _kernels/__init__.py:63-68 jet_act_backward (_cyjet.pyx:37-86)
+ */
+#ifndef FLOWREC_B200_H
+#define FLOWREC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fr_stream_t; /* == cudaStream_t */
+typedef struct fr_plan fr_plan;
+
+enum { FR_ACT_TANH = 0, FR_ACT_SIN = 1 };                                /* _kernels ACT_* */
+enum { FR_STEADY2D = 0, FR_UNSTEADY2D = 1, FR_UNSTEADY3D = 2 };          /* physics._KINDS */
+enum { FR_F32 = 0, FR_F64 = 1 };
+enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3 };
+enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2 };
+
+typedef struct {
+  int n_in, n_out, n_vel, hidden_layers, width, width_pad;
+  int n_params;      /* reference flat parameter count (network.py:112-115) */
+  int np_pad;        /* kernel gradient-partial row length */
+  int kp_elems;      /* elements of the prepared kernel-parameter buffer */
+  int dtype, act, regime, num_sms;
+  double inv_re;
+} fr_plan_info;
+
+typedef struct {
+  int grid;           /* CTAs == gradient / loss partial rows written */
+  int threads;        /* threads per CTA */
+  int points_per_tile;
+  int jet_streams;    /* rows per point in JET mode output (n, S, n_out) */
+  long long gpart_elems;   /* doubles: grid * np_pad (0 for forward-only modes) */
+  long long lpart_elems;   /* doubles: grid * 2 */
+  long long scratch_bytes; /* per-call stash workspace */
+  size_t smem_bytes;
+} fr_workspace;
+
+/* Plan: validated network + regime description (replaces per-bind checks). */
+int fr_plan_create(const int* arch, int n_arch, int act, int regime, double inv_re, int dtype,
+                   fr_plan** out);
+int fr_plan_destroy(fr_plan* plan);
+int fr_plan_get_info(const fr_plan* plan, fr_plan_info* out);
+int fr_plan_workspace(const fr_plan* plan, int mode, long long n, fr_workspace* out);
+
+/* flat f64 params (reference layout) -> padded kernel params (+ W^T copies) */
+int fr_prepare_params(const fr_plan* plan, const double* flat, void* kparams, fr_stream_t stream);
+
+/* PDE residual loss over n collocation points: per-CTA f64 gradient partials of
+ * coef * sum_n |r_n|^2 and per-CTA f64 sums of |r_n|^2 (lpart[2*cta]). */
+int fr_pde_fwd_bwd(const fr_plan* plan, const void* kparams, const void* pts, long long n,
+                   double coef, double* gpart, double* lpart, void* scratch, fr_stream_t stream);
+
+/* MSE head: vel_coef * sum_n sum_c w_c (u_c - tu_c)^2 + p_coef * sum_n (p - tp)^2;
+ * target_p == NULL omits the pressure term (builders.py:133-139). */
+int fr_mse_fwd_bwd(const fr_plan* plan, const void* kparams, const void* pts, const void* target_u,
+                   const void* target_p, long long n, const double* vel_w, double vel_coef,
+                   double p_coef, double* gpart, double* lpart, void* scratch, fr_stream_t stream);
+
+/* value forward: out (n, n_out) */
+int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,
+                 fr_stream_t stream);
+/* jet forward: out (n, 1 + 2*n_in, n_out): value, d/dx_j, d2/dx_j^2 */
+int fr_jet_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,
+               fr_stream_t stream);
+
+/* grad[i] (+)= sum_rows gpart[row][pad(i)], fixed row order */
+int fr_reduce_grad(const fr_plan* plan, const double* gpart, int rows, double* grad, int accumulate,
+                   fr_stream_t stream);
+/* sums[2*s + c] = sum over rows of segment s of lpart[2*row + c], fixed order */
+int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int n_seg, double* sums,
+                   fr_stream_t stream);
+
+typedef struct {
+  /* optimiser state (device, f64, length n) */
+  long long n;
+  double* params;
+  double* grad;
+  double* m;
+  double* v;
+  long long* step;          /* device counter, AdamState.step */
+  /* schedule: row r = *step - row_base holds {lr, 1 - beta1^t, 1 - beta2^t} for
+   * t = *step + 1 (host-computed, bit-identical to the reference's Python float
+   * math); history and grad_norm rows use the same index r */
+  const double* sched;
+  long long row_base;
+  double beta1, beta2, eps, clip_norm; /* clip_norm <= 0: no clipping */
+  /* loss bookkeeping (NULL -> no history / finiteness check): fr_reduce_loss
+   * output over the segments {obs, pde, ghost-spatial, ghost-temporal}, i.e.
+   * sums[8] = {obs sq_u, -, pde sq, -, gs sq_u, gs sq_p, gt sq_u, gt sq_p} */
+  const double* loss_sums;
+  double n_obs, n_colloc, n_ghost_total, n_ghost_space, n_ghost_time;
+  double w_obs, w_pde, w_ghost_u, w_ghost_p_space, w_ghost_p_time;
+  double* history;          /* rows of 7: epoch, 5 unweighted parts, lr */
+  int* flags;               /* FR_FLAG_* bits, sticky */
+  double* grad_norm;        /* optional: pre-clip norm per step (indexed by step) */
+  /* optional: refresh prepared kernel params after the update */
+  void* kparams;
+} fr_adam_args;
+
+/* plan may be NULL when kparams is NULL (plain flat-vector Adam) */
+int fr_adam_step(const fr_plan* plan, const fr_adam_args* args, fr_stream_t stream);
+
+/* ghost message: u = y[:, :n_vel]; p = y[:, p] - (y_anchor ? y_anchor[:, p] : 0) */
+int fr_pack_ghost(const fr_plan* plan, const void* y, const void* y_anchor, long long n, void* out_u,
+                  void* out_p, fr_stream_t stream);
+
+/* The reference's native seam (f64, stacked layout ((1+2d)*batch, width)). */
+int fr_jet_act_forward(int kind, const double* z, double* s, const double* aux, double* d1,
+                       double* d2, long long batch, int n_inputs, int width, fr_stream_t stream);
+int fr_jet_act_backward(int kind, const double* z, const double* s, const double* aux,
+                        const double* sbar, double* zbar, long long batch, int n_inputs, int width,
+                        int accumulate, fr_stream_t stream);
+
+/* FP32 FFMA throughput probe (measured SIMT roofline denominator): grid x 256
+ * threads, each running `iters` x 64 independent FMA chains of 8; out[grid*256] */
+int fr_bench_ffma(int grid, int iters, int unused, float* out, fr_stream_t stream);
+
+const char* fr_last_error(void);
+const char* fr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWREC_B200_H */

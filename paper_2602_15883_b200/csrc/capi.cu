@@ -1,0 +1,564 @@
+// C ABI: plan, parameter preparation, reductions, Adam, ghost packing, and the
+// reference's activation-jet seam.  See include/flowrec_b200.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/flowrec_b200.h"
+#include "jetmlp_dispatch.cuh"
+
+namespace fr {
+int mode_entry_PDE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+int mode_entry_MSE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+int mode_entry_VALUE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+int mode_entry_JET(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+}  // namespace fr
+
+using namespace fr;
+
+static thread_local std::string g_err;
+
+static int fail(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
+static int fail(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return 1;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail("%s: CUDA error %d (%s)", where, int(e), cudaGetErrorString(e));
+}
+#define FR_CUDA(call, where)                        \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+struct fr_plan {
+  fr_plan_info info;
+  ParamLayout pl;
+  int* d_map = nullptr;      // real flat index -> padded index      [n_params]
+  int* d_inv = nullptr;      // kernel-param element -> real index or -1 [kp_elems]
+};
+
+extern "C" const char* fr_last_error(void) { return g_err.c_str(); }
+extern "C" const char* fr_version(void) { return "flowrec_b200 0.1.0 sm_100a"; }
+
+static int regime_dims(int regime, int* din, int* nout, int* nvel) {
+  switch (regime) {
+    case FR_STEADY2D: *din = 2; *nout = 3; *nvel = 2; return 0;
+    case FR_UNSTEADY2D: *din = 3; *nout = 3; *nvel = 2; return 0;
+    case FR_UNSTEADY3D: *din = 4; *nout = 4; *nvel = 3; return 0;
+    default: return 1;
+  }
+}
+
+extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, double inv_re, int dtype,
+                              fr_plan** out) {
+  if (!out) return fail("fr_plan_create: out is NULL");
+  *out = nullptr;
+  if (!arch || n_arch < 3) return fail("architecture needs at least one hidden layer (got %d entries)", n_arch);
+  for (int i = 0; i < n_arch; ++i)
+    if (arch[i] < 1) return fail("zero-width layer in architecture (entry %d = %d)", i, arch[i]);
+  if (act != FR_ACT_TANH && act != FR_ACT_SIN) return fail("unsupported activation kind %d", act);
+  if (dtype != FR_F32 && dtype != FR_F64) return fail("unsupported dtype %d", dtype);
+  int din, nout, nvel;
+  if (regime_dims(regime, &din, &nout, &nvel)) return fail("unknown regime kind %d", regime);
+  if (arch[0] != din) return fail("regime expects %d inputs, architecture has %d", din, arch[0]);
+  if (arch[n_arch - 1] != nout)
+    return fail("regime expects %d outputs, architecture has %d", nout, arch[n_arch - 1]);
+  const int width = arch[1];
+  for (int i = 1; i < n_arch - 1; ++i)
+    if (arch[i] != width) return fail("hidden layers must share one width (ExpertConfig); got %d and %d", width, arch[i]);
+  int wpad;
+  if (width <= 16) wpad = 16;
+  else if (width <= 32) wpad = 32;
+  else if (width <= 64) wpad = 64;
+  else return fail("hidden width %d > 64 is not supported by the SIMT kernels", width);
+  if (!(inv_re > 0.0) || !std::isfinite(inv_re)) return fail("inv_re must be positive and finite");
+
+  fr_plan* p = new fr_plan();
+  fr_plan_info& I = p->info;
+  I.n_in = din; I.n_out = nout; I.n_vel = nvel;
+  I.hidden_layers = n_arch - 2; I.width = width; I.width_pad = wpad;
+  I.dtype = dtype; I.act = act; I.regime = regime; I.inv_re = inv_re;
+  const int L = I.hidden_layers;
+  p->pl = ParamLayout{din, wpad, nout, L};
+  I.np_pad = p->pl.np_pad();
+  I.kp_elems = p->pl.total();
+  // real flat layout W0,b0,W1,b1,... (network.py:112-115)
+  std::vector<int> map;
+  std::vector<int> inv(I.kp_elems, -1);
+  for (int l = 0; l <= L; ++l) {
+    const int fi = (l == 0) ? din : width;
+    const int fo = (l == L) ? nout : width;
+    const int fo_pad = (l == L) ? nout : wpad;
+    for (int i = 0; i < fi; ++i)
+      for (int o = 0; o < fo; ++o) {
+        const int pidx = p->pl.off_w(l) + i * fo_pad + o;
+        inv[pidx] = int(map.size());
+        if (l >= 1 && l < L) inv[p->pl.off_wt(l) + o * wpad + i] = int(map.size());
+        map.push_back(pidx);
+      }
+    for (int o = 0; o < fo; ++o) {
+      const int pidx = p->pl.off_b(l) + o;
+      inv[pidx] = int(map.size());
+      map.push_back(pidx);
+    }
+  }
+  I.n_params = int(map.size());
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&I.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_map, sizeof(int) * map.size());
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_inv, sizeof(int) * inv.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_map, map.data(), sizeof(int) * map.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_inv, inv.data(), sizeof(int) * inv.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(p->d_map);
+    cudaFree(p->d_inv);
+    delete p;
+    return cuda_fail(e, "fr_plan_create");
+  }
+  *out = p;
+  return 0;
+}
+
+extern "C" int fr_plan_destroy(fr_plan* p) {
+  if (!p) return 0;
+  cudaFree(p->d_map);
+  cudaFree(p->d_inv);
+  delete p;
+  return 0;
+}
+
+extern "C" int fr_plan_get_info(const fr_plan* p, fr_plan_info* out) {
+  if (!p || !out) return fail("fr_plan_get_info: NULL argument");
+  *out = p->info;
+  return 0;
+}
+
+static int mode_call(const fr_plan* p, int mode, const KArgs* a, int grid, cudaStream_t st, KInfo* info) {
+  const fr_plan_info& I = p->info;
+  int r;
+  switch (mode) {
+    case FR_MODE_PDE: r = mode_entry_PDE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
+    case FR_MODE_MSE: r = mode_entry_MSE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
+    case FR_MODE_VALUE: r = mode_entry_VALUE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
+    case FR_MODE_JET: r = mode_entry_JET(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
+    default: return fail("unknown mode %d", mode);
+  }
+  if (r == -1) return fail("kernel variant not compiled (mode %d dtype %d act %d regime %d width %d)", mode, I.dtype, I.act, I.regime, I.width_pad);
+  if (r != 0) return cuda_fail(cudaError_t(r), "jet-MLP kernel launch");
+  return 0;
+}
+
+extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_workspace* out) {
+  if (!p || !out) return fail("fr_plan_workspace: NULL argument");
+  if (n < 0) return fail("negative point count");
+  KInfo ki{};
+  if (mode_call(p, mode, nullptr, 0, nullptr, &ki)) return 1;
+  const fr_plan_info& I = p->info;
+  const long long ntiles = (n + ki.ppt - 1) / ki.ppt;
+  const int sms = I.num_sms > 0 ? I.num_sms : 148;
+  out->grid = int(ntiles < sms ? ntiles : sms);
+  out->threads = ki.nt;
+  out->points_per_tile = ki.ppt;
+  out->jet_streams = 1 + 2 * I.n_in;
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  out->gpart_elems = bwd ? (long long)out->grid * I.np_pad : 0;
+  out->lpart_elems = bwd ? (long long)out->grid * 2 : 0;
+  const size_t esz = I.dtype == FR_F32 ? 4 : 8;
+  out->scratch_bytes = bwd ? (long long)out->grid * ki.stash_elems * (long long)esz : 0;
+  out->smem_bytes = ki.smem;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void prepare_kernel(const double* __restrict__ flat, const int* __restrict__ inv, T* kp, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = inv[i];
+    kp[i] = r >= 0 ? T(flat[r]) : T(0);
+  }
+}
+
+extern "C" int fr_prepare_params(const fr_plan* p, const double* flat, void* kparams, fr_stream_t stream) {
+  if (!p || !flat || !kparams) return fail("fr_prepare_params: NULL argument");
+  const int n = p->info.kp_elems;
+  const int blocks = (n + 255) / 256;
+  if (p->info.dtype == FR_F32)
+    prepare_kernel<float><<<blocks, 256, 0, stream>>>(flat, p->d_inv, static_cast<float*>(kparams), n);
+  else
+    prepare_kernel<double><<<blocks, 256, 0, stream>>>(flat, p->d_inv, static_cast<double*>(kparams), n);
+  FR_CUDA(cudaGetLastError(), "fr_prepare_params");
+  return 0;
+}
+
+static int launch_train(const fr_plan* p, int mode, KArgs& a, long long n, cudaStream_t st) {
+  fr_workspace ws;
+  if (fr_plan_workspace(p, mode, n, &ws)) return 1;
+  a.n = n;
+  a.L = p->info.hidden_layers;
+  a.np_pad = p->info.np_pad;
+  KInfo ki{};
+  if (mode_call(p, mode, nullptr, 0, nullptr, &ki)) return 1;
+  a.stash_elems = ki.stash_elems;
+  a.inv_re = p->info.inv_re;
+  if (ws.grid == 0) return 0;
+  return mode_call(p, mode, &a, ws.grid, st, nullptr);
+}
+
+extern "C" int fr_pde_fwd_bwd(const fr_plan* p, const void* kparams, const void* pts, long long n, double coef,
+                              double* gpart, double* lpart, void* scratch, fr_stream_t stream) {
+  if (!p || !kparams || (n > 0 && (!pts || !gpart || !lpart || !scratch)))
+    return fail("fr_pde_fwd_bwd: NULL argument");
+  if (n < 0) return fail("fr_pde_fwd_bwd: negative point count");
+  KArgs a{};
+  a.kp = kparams; a.pts = pts; a.gpart = gpart; a.lpart = lpart; a.scratch = scratch;
+  a.coef = coef;
+  return launch_train(p, FR_MODE_PDE, a, n, stream);
+}
+
+extern "C" int fr_mse_fwd_bwd(const fr_plan* p, const void* kparams, const void* pts, const void* target_u,
+                              const void* target_p, long long n, const double* vel_w, double vel_coef,
+                              double p_coef, double* gpart, double* lpart, void* scratch, fr_stream_t stream) {
+  if (!p || !kparams || (n > 0 && (!pts || !target_u || !gpart || !lpart || !scratch)))
+    return fail("fr_mse_fwd_bwd: NULL argument");
+  if (n < 0) return fail("fr_mse_fwd_bwd: negative point count");
+  KArgs a{};
+  a.kp = kparams; a.pts = pts; a.tu = target_u; a.tp = target_p;
+  a.gpart = gpart; a.lpart = lpart; a.scratch = scratch;
+  a.coef = vel_coef; a.pcoef = p_coef; a.has_p = target_p != nullptr;
+  for (int c = 0; c < 4; ++c) a.velw[c] = 1.0;
+  if (vel_w)
+    for (int c = 0; c < p->info.n_vel; ++c) a.velw[c] = vel_w[c];
+  return launch_train(p, FR_MODE_MSE, a, n, stream);
+}
+
+extern "C" int fr_value_fwd(const fr_plan* p, const void* kparams, const void* pts, long long n, void* out,
+                            fr_stream_t stream) {
+  if (!p || !kparams || (n > 0 && (!pts || !out))) return fail("fr_value_fwd: NULL argument");
+  KArgs a{};
+  a.kp = kparams; a.pts = pts; a.out = out;
+  return launch_train(p, FR_MODE_VALUE, a, n, stream);
+}
+
+extern "C" int fr_jet_fwd(const fr_plan* p, const void* kparams, const void* pts, long long n, void* out,
+                          fr_stream_t stream) {
+  if (!p || !kparams || (n > 0 && (!pts || !out))) return fail("fr_jet_fwd: NULL argument");
+  KArgs a{};
+  a.kp = kparams; a.pts = pts; a.out = out;
+  return launch_train(p, FR_MODE_JET, a, n, stream);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void reduce_grad_kernel(const double* __restrict__ gpart, int rows, int np_pad, const int* __restrict__ map,
+                                   int n, double* grad, int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int col = map[i];
+  double s = 0.0;
+  for (int r = 0; r < rows; ++r) s += gpart[size_t(r) * np_pad + col];
+  grad[i] = accumulate ? grad[i] + s : s;
+}
+
+extern "C" int fr_reduce_grad(const fr_plan* p, const double* gpart, int rows, double* grad, int accumulate,
+                              fr_stream_t stream) {
+  if (!p || !grad || (rows > 0 && !gpart)) return fail("fr_reduce_grad: NULL argument");
+  const int n = p->info.n_params;
+  if (rows <= 0 && accumulate) return 0;
+  reduce_grad_kernel<<<(n + 127) / 128, 128, 0, stream>>>(gpart, rows > 0 ? rows : 0, p->info.np_pad, p->d_map, n,
+                                                          grad, accumulate);
+  FR_CUDA(cudaGetLastError(), "fr_reduce_grad");
+  return 0;
+}
+
+struct SegRows {
+  int n;
+  int rows[8];
+};
+__global__ void reduce_loss_kernel(const double* __restrict__ lpart, SegRows seg, double* sums) {
+  const int s = threadIdx.x;
+  if (s >= seg.n) return;
+  int r0 = 0;
+  for (int i = 0; i < s; ++i) r0 += seg.rows[i];
+  double a = 0.0, b = 0.0;
+  for (int r = r0; r < r0 + seg.rows[s]; ++r) {
+    a += lpart[2 * r];
+    b += lpart[2 * r + 1];
+  }
+  sums[2 * s] = a;
+  sums[2 * s + 1] = b;
+}
+
+extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int n_seg, double* sums,
+                              fr_stream_t stream) {
+  if (!sums || !seg_rows_host || n_seg < 1 || n_seg > 8) return fail("fr_reduce_loss: bad arguments");
+  SegRows seg{};
+  seg.n = n_seg;
+  int total = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    seg.rows[i] = seg_rows_host[i];
+    total += seg_rows_host[i];
+  }
+  if (total > 0 && !lpart) return fail("fr_reduce_loss: NULL lpart");
+  reduce_loss_kernel<<<1, 32, 0, stream>>>(lpart, seg, sums);
+  FR_CUDA(cudaGetLastError(), "fr_reduce_loss");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Adam (optim.py:20-49) with the epoch bookkeeping of objective.py:183-198 and
+// worker.py:231-244.  One CTA; every reduction in a fixed order.  f64 products
+// and sums use explicit round-to-nearest intrinsics so no FMA contraction
+// changes the reference's rounding sequence.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024) adam_kernel(fr_adam_args a, int n, const int* __restrict__ inv, int kp_elems) {
+  __shared__ double red[1024];
+  __shared__ int skip;
+  const int tid = threadIdx.x;
+  const long long step0 = *a.step;  // steps taken so far
+  const long long row = step0 - a.row_base;
+  if (tid == 0) {
+    skip = 0;
+    if (a.loss_sums) {
+      const double* s = a.loss_sums;
+      const double obs = a.n_obs > 0 ? s[0] / a.n_obs : 0.0;
+      const double pde = s[2] / a.n_colloc;
+      const double gu = a.n_ghost_total > 0 ? (s[4] + s[6]) / a.n_ghost_total : 0.0;
+      const double gps = a.n_ghost_space > 0 ? s[5] / a.n_ghost_space : 0.0;
+      const double gpt = a.n_ghost_time > 0 ? s[7] / a.n_ghost_time : 0.0;
+      // compose_loss (physics.py:214-224), evaluated left to right
+      double total = __dmul_rn(a.w_obs, obs);
+      total = __dadd_rn(total, __dmul_rn(a.w_pde, pde));
+      total = __dadd_rn(total, __dmul_rn(a.w_ghost_u, gu));
+      total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_space, gps));
+      total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_time, gpt));
+      if (a.history) {
+        double* h = a.history + 7 * row;
+        h[0] = double(step0);
+        h[1] = obs; h[2] = pde; h[3] = gu; h[4] = gps; h[5] = gpt;
+        h[6] = a.sched[3 * row];
+      }
+      if (!isfinite(total)) {
+        atomicOr(a.flags, FR_FLAG_NONFINITE_LOSS);
+        skip = 1;
+      }
+    }
+  }
+  double acc = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) acc = __dadd_rn(acc, __dmul_rn(a.grad[i], a.grad[i]));
+  red[tid] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] = __dadd_rn(red[tid], red[tid + w]);
+    __syncthreads();
+  }
+  const double norm = sqrt(red[0]);
+  if (tid == 0 && a.grad_norm) a.grad_norm[row] = norm;
+  if (!isfinite(norm)) {
+    if (tid == 0) atomicOr(a.flags, FR_FLAG_NONFINITE_GRAD);
+    return;
+  }
+  if (skip) return;
+  const double scale = (a.clip_norm > 0.0 && norm > a.clip_norm) ? a.clip_norm / norm : 1.0;
+  const double lr = a.sched[3 * row];
+  const double bc1 = a.sched[3 * row + 1];
+  const double bc2 = a.sched[3 * row + 2];
+  const double omb1 = 1.0 - a.beta1, omb2 = 1.0 - a.beta2;
+  for (int i = tid; i < n; i += blockDim.x) {
+    double g = a.grad[i];
+    if (scale != 1.0) {
+      g = __dmul_rn(g, scale);
+      a.grad[i] = g;
+    }
+    double m = __dadd_rn(__dmul_rn(a.m[i], a.beta1), __dmul_rn(omb1, g));
+    double v = __dadd_rn(__dmul_rn(a.v[i], a.beta2), __dmul_rn(__dmul_rn(omb2, g), g));
+    a.m[i] = m;
+    a.v[i] = v;
+    const double mh = __ddiv_rn(m, bc1);
+    const double vh = __ddiv_rn(v, bc2);
+    const double upd = __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), a.eps));
+    a.params[i] = __dsub_rn(a.params[i], upd);
+  }
+  __syncthreads();
+  if (tid == 0) *a.step = step0 + 1;
+  if (a.kparams) {
+    T* kp = static_cast<T*>(a.kparams);
+    for (int i = tid; i < kp_elems; i += blockDim.x) {
+      const int r = inv[i];
+      if (r >= 0) kp[i] = T(a.params[r]);
+    }
+  }
+}
+
+extern "C" int fr_adam_step(const fr_plan* p, const fr_adam_args* args, fr_stream_t stream) {
+  if (!args || !args->params || !args->grad || !args->m || !args->v || !args->step || !args->sched ||
+      !args->flags)
+    return fail("fr_adam_step: NULL argument");
+  if (args->n < 1 || args->n > (1LL << 30)) return fail("fr_adam_step: bad parameter count %lld", args->n);
+  if (args->kparams && !p) return fail("fr_adam_step: refreshing kernel params needs the plan");
+  if (p && args->n != p->info.n_params)
+    return fail("fr_adam_step: n=%lld does not match the plan's %d parameters", args->n, p->info.n_params);
+  if (args->loss_sums && !(args->n_colloc > 0)) return fail("fr_adam_step: n_colloc must be positive");
+  const int* inv = p ? p->d_inv : nullptr;
+  const int kpe = p ? p->info.kp_elems : 0;
+  if (!p || p->info.dtype == FR_F32)
+    adam_kernel<float><<<1, 1024, 0, stream>>>(*args, int(args->n), inv, kpe);
+  else
+    adam_kernel<double><<<1, 1024, 0, stream>>>(*args, int(args->n), inv, kpe);
+  FR_CUDA(cudaGetLastError(), "fr_adam_step");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void pack_ghost_kernel(const T* __restrict__ y, const T* __restrict__ ya, long long n, int nout,
+                                  int nvel, T* out_u, T* out_p) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    for (int c = 0; c < nvel; ++c) out_u[i * nvel + c] = y[i * nout + c];
+    const T pv = y[i * nout + nvel];
+    out_p[i] = ya ? pv - ya[i * nout + nvel] : pv;
+  }
+}
+
+extern "C" int fr_pack_ghost(const fr_plan* p, const void* y, const void* y_anchor, long long n, void* out_u,
+                             void* out_p, fr_stream_t stream) {
+  if (!p || (n > 0 && (!y || !out_u || !out_p))) return fail("fr_pack_ghost: NULL argument");
+  if (n <= 0) return 0;
+  const int blocks = int((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  if (p->info.dtype == FR_F32)
+    pack_ghost_kernel<float><<<blocks, 256, 0, stream>>>(static_cast<const float*>(y), static_cast<const float*>(y_anchor), n,
+                                                         p->info.n_out, p->info.n_vel, static_cast<float*>(out_u),
+                                                         static_cast<float*>(out_p));
+  else
+    pack_ghost_kernel<double><<<blocks, 256, 0, stream>>>(static_cast<const double*>(y), static_cast<const double*>(y_anchor),
+                                                          n, p->info.n_out, p->info.n_vel, static_cast<double*>(out_u),
+                                                          static_cast<double*>(out_p));
+  FR_CUDA(cudaGetLastError(), "fr_pack_ghost");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Reference seam (_kernels): elementwise jet propagation on stacked f64 arrays
+// ((1 + 2d) * batch, width).  Semantics of numpy_backend.py:43-89, including
+// "written" (accumulate=0) versus "added" adjoints.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void factors(int kind, double s, double c, double* d1, double* d2, double* d3) {
+  if (kind == FR_ACT_TANH) {
+    *d1 = __dsub_rn(1.0, __dmul_rn(s, s));
+    *d2 = __dmul_rn(__dmul_rn(s, *d1), -2.0);
+    if (d3) *d3 = __dmul_rn(__dadd_rn(__dmul_rn(*d1, *d1), __dmul_rn(s, *d2)), -2.0);
+  } else {
+    *d1 = c;
+    *d2 = -s;
+    if (d3) *d3 = -c;
+  }
+}
+
+__global__ void act_fwd_kernel(int kind, const double* z, double* s, const double* aux, double* d1o, double* d2o,
+                               long long batch, int d, int width) {
+  const long long total = batch * width;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const double sv = s[e];
+    double d1, d2;
+    factors(kind, sv, kind == FR_ACT_TANH ? 0.0 : aux[e], &d1, &d2, nullptr);
+    d1o[e] = d1;
+    d2o[e] = d2;
+    for (int j = 0; j < d; ++j) {
+      const long long gi = (1 + j) * total + e;
+      const long long li = (1 + d + j) * total + e;
+      const double zg = z[gi];
+      s[gi] = __dmul_rn(d1, zg);
+      s[li] = __dadd_rn(__dmul_rn(__dmul_rn(d2, zg), zg), __dmul_rn(d1, z[li]));
+    }
+  }
+}
+
+__global__ void act_bwd_kernel(int kind, const double* z, const double* s, const double* aux, const double* sbar,
+                               double* zbar, long long batch, int d, int width, int accumulate) {
+  const long long total = batch * width;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    double d1, d2, d3;
+    factors(kind, s[e], kind == FR_ACT_TANH ? 0.0 : aux[e], &d1, &d2, &d3);
+    double acc = __dmul_rn(sbar[e], d1);
+    for (int j = 0; j < d; ++j) {
+      const long long gi = (1 + j) * total + e;
+      const long long li = (1 + d + j) * total + e;
+      const double zg = z[gi], sg = sbar[gi], sl = sbar[li];
+      const double t1 = __dmul_rn(sg, __dmul_rn(d2, zg));
+      const double t2 = __dmul_rn(sl, __dadd_rn(__dmul_rn(__dmul_rn(d3, zg), zg), __dmul_rn(d2, z[li])));
+      acc = __dadd_rn(acc, __dadd_rn(t1, t2));
+      const double tg = __dadd_rn(__dmul_rn(sg, d1), __dmul_rn(__dmul_rn(__dmul_rn(2.0, d2), zg), sl));
+      const double tl = __dmul_rn(sl, d1);
+      zbar[gi] = accumulate ? __dadd_rn(zbar[gi], tg) : tg;
+      zbar[li] = accumulate ? __dadd_rn(zbar[li], tl) : tl;
+    }
+    zbar[e] = accumulate ? __dadd_rn(zbar[e], acc) : acc;
+  }
+}
+
+extern "C" int fr_jet_act_forward(int kind, const double* z, double* s, const double* aux, double* d1, double* d2,
+                                  long long batch, int n_inputs, int width, fr_stream_t stream) {
+  if (kind != FR_ACT_TANH && kind != FR_ACT_SIN) return fail("unknown activation kind %d", kind);
+  if (!z || !s || !d1 || !d2 || (kind == FR_ACT_SIN && !aux)) return fail("fr_jet_act_forward: NULL argument");
+  if (batch < 0 || n_inputs < 0 || width < 1) return fail("fr_jet_act_forward: bad shape");
+  const long long total = batch * width;
+  if (total == 0) return 0;
+  const int blocks = int((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  act_fwd_kernel<<<blocks, 256, 0, stream>>>(kind, z, s, aux, d1, d2, batch, n_inputs, width);
+  FR_CUDA(cudaGetLastError(), "fr_jet_act_forward");
+  return 0;
+}
+
+extern "C" int fr_jet_act_backward(int kind, const double* z, const double* s, const double* aux, const double* sbar,
+                                   double* zbar, long long batch, int n_inputs, int width, int accumulate,
+                                   fr_stream_t stream) {
+  if (kind != FR_ACT_TANH && kind != FR_ACT_SIN) return fail("unknown activation kind %d", kind);
+  if (!z || !s || !sbar || !zbar || (kind == FR_ACT_SIN && !aux)) return fail("fr_jet_act_backward: NULL argument");
+  if (batch < 0 || n_inputs < 0 || width < 1) return fail("fr_jet_act_backward: bad shape");
+  const long long total = batch * width;
+  if (total == 0) return 0;
+  const int blocks = int((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  act_bwd_kernel<<<blocks, 256, 0, stream>>>(kind, z, s, aux, sbar, zbar, batch, n_inputs, width, accumulate);
+  FR_CUDA(cudaGetLastError(), "fr_jet_act_backward");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// FP32 FFMA probe: 16 independent accumulators per thread, 4 FMAs per operand
+// load-free inner step; measures the SIMT FP32 roofline on this part.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ffma_kernel(int iters, float* out) {
+  float a[16];
+  const float x = 1.0f + 1e-7f * threadIdx.x, y = 0.999999f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = float(i) * 1e-3f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], y, x);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+extern "C" int fr_bench_ffma(int grid, int iters, int, float* out, fr_stream_t stream) {
+  if (grid < 1 || iters < 1 || !out) return fail("fr_bench_ffma: bad arguments");
+  ffma_kernel<<<grid, 256, 0, stream>>>(iters, out);
+  FR_CUDA(cudaGetLastError(), "fr_bench_ffma");
+  return 0;
+}

@@ -1,0 +1,3 @@
+// Instantiations of the fused jet-MLP kernel for MODE_JET.
+#include "jetmlp_dispatch.cuh"
+FR_DEFINE_MODE_ENTRY(JET)

@@ -1,0 +1,801 @@
+// Kernel template bodies (included by the per-mode translation units).
+#pragma once
+#include "jetmlp.cuh"
+
+namespace fr {
+
+// ---------------------------------------------------------------------------
+// scalar math (accurate libm versions: first-layer arguments reach |z|~17 on
+// the cylinder box, so tanh.approx / __sinf are not acceptable)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float tanh_t(float x) { return tanhf(x); }
+__device__ __forceinline__ double tanh_t(double x) { return tanh(x); }
+__device__ __forceinline__ void sincos_t(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void sincos_t(double x, double* s, double* c) { sincos(x, s, c); }
+
+// sigma and its derivative factors (numpy_backend.py:23-40)
+template <int ACT, typename T>
+__device__ __forceinline__ void act_eval(T z, T& s, T& c) {
+  if constexpr (ACT == ACT_TANH) {
+    s = tanh_t(z);
+    c = T(0);
+  } else {
+    sincos_t(z, &s, &c);
+  }
+}
+template <int ACT, typename T>
+__device__ __forceinline__ void act_d12(T s, T c, T& d1, T& d2) {
+  if constexpr (ACT == ACT_TANH) {
+    d1 = T(1) - s * s;
+    d2 = (s * d1) * T(-2);
+  } else {
+    d1 = c;
+    d2 = -s;
+  }
+}
+template <int ACT, typename T>
+__device__ __forceinline__ T act_d3(T s, T c, T d1, T d2) {
+  if constexpr (ACT == ACT_TANH) {
+    return (d1 * d1 + s * d2) * T(-2);
+  } else {
+    return -c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vectorised shared-memory block copies
+// ---------------------------------------------------------------------------
+template <typename T, int N>
+struct VecW {
+  static constexpr int V =
+      sizeof(T) == 4 ? ((N % 4 == 0) ? 4 : ((N % 2 == 0) ? 2 : 1)) : ((N % 2 == 0) ? 2 : 1);
+};
+
+template <typename T, int N>
+__device__ __forceinline__ void vload(T (&dst)[N], const T* src) {
+  constexpr int V = VecW<T, N>::V;
+#pragma unroll
+  for (int i = 0; i < N; i += V) {
+    if constexpr (sizeof(T) == 4 && V == 4) {
+      float4 v = *reinterpret_cast<const float4*>(src + i);
+      dst[i] = v.x; dst[i + 1] = v.y; dst[i + 2] = v.z; dst[i + 3] = v.w;
+    } else if constexpr (sizeof(T) == 4 && V == 2) {
+      float2 v = *reinterpret_cast<const float2*>(src + i);
+      dst[i] = v.x; dst[i + 1] = v.y;
+    } else if constexpr (sizeof(T) == 8 && V == 2) {
+      double2 v = *reinterpret_cast<const double2*>(src + i);
+      dst[i] = v.x; dst[i + 1] = v.y;
+    } else {
+      dst[i] = src[i];
+    }
+  }
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void vstore(T* dst, const T (&src)[N]) {
+  constexpr int V = VecW<T, N>::V;
+#pragma unroll
+  for (int i = 0; i < N; i += V) {
+    if constexpr (sizeof(T) == 4 && V == 4) {
+      *reinterpret_cast<float4*>(dst + i) = make_float4(src[i], src[i + 1], src[i + 2], src[i + 3]);
+    } else if constexpr (sizeof(T) == 4 && V == 2) {
+      *reinterpret_cast<float2*>(dst + i) = make_float2(src[i], src[i + 1]);
+    } else if constexpr (sizeof(T) == 8 && V == 2) {
+      *reinterpret_cast<double2*>(dst + i) = make_double2(src[i], src[i + 1]);
+    } else {
+      dst[i] = src[i];
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// compile-time configuration
+// ---------------------------------------------------------------------------
+template <typename T, int ACT, int MODE, int REG, int W>
+struct JetCfg {
+  using R = Regime<REG>;
+  using St = Streams<MODE, REG>;
+  static constexpr int DIN = R::DIN, NOUT = R::NOUT, NVEL = R::NVEL, HAS_T = R::HAS_T;
+  static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0, RPT = St::RPT;
+  static constexpr bool JET = St::JET;
+  static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE);
+  static constexpr int NT = sizeof(T) == 4 ? 256 : 128;
+  static constexpr int G = W / 8;          // unit groups of 8 per row group
+  static constexpr int NRG = NT / G;       // row groups
+  static constexpr int ROWS = NRG * RPT;   // rows per tile
+  static constexpr int PPT = JET ? NRG : ROWS;  // points per tile
+  static constexpr int PP = JET ? 1 : RPT;      // points per thread
+  static constexpr int SIN = (ACT == ACT_SIN) ? 1 : 0;
+  static constexpr int NST0 = 1 + SIN;                       // layer-0 stash / (point,unit)
+  static constexpr int NSTH = JET ? (1 + SIN + NG + NL) : NST0;  // hidden-layer stash
+  static constexpr int RS2_BASE = 2 * ROWS;
+  static constexpr int RS2 = sizeof(T) == 4 ? RS2_BASE + ((4 - RS2_BASE % 32) + 32) % 32
+                                            : RS2_BASE + ((2 - RS2_BASE % 16) + 16) % 16;
+  static constexpr int XELEMS = (W / 2) * RS2;
+  static_assert(W % 8 == 0, "width must be a multiple of 8");
+  static_assert(NT % G == 0, "thread count must be divisible by unit groups");
+  static_assert(ROWS % 2 == 0, "tile rows must be even");
+
+  __host__ __device__ static int stash_per_thread(int L) { return 8 * PP * (NST0 + (L - 1) * NSTH); }
+  __host__ __device__ static int stash_layer_base(int l) {
+    return l == 0 ? 0 : 8 * PP * (NST0 + (l - 1) * NSTH);
+  }
+  // shared memory carve (elements of T), all blocks 16-byte aligned
+  __host__ __device__ static constexpr int al(int n) { return (n + 3) & ~3; }
+  __host__ __device__ static int smem_elems(int L) {
+    int e = 0;
+    e += al(XELEMS);                       // Xs
+    if (BWD) e += al(XELEMS);              // Gs
+    e += 2 * W * W;                        // weight slots
+    e += al(DIN * W);                      // W0s
+    e += al(L * W);                        // hidden biases
+    e += al(W * NOUT);                     // WLs
+    e += 4;                                // bLs
+    e += al(ROWS * NOUT);                  // Ys
+    if (BWD) e += al(ROWS * NOUT);         // Ybs
+    e += al(PPT * DIN);                    // Ps
+    if (MODE == MODE_MSE) e += al(PPT * NVEL) + al(PPT);  // targets
+    return e;
+  }
+  __host__ __device__ static size_t smem_bytes(int L) {
+    return size_t(smem_elems(L)) * sizeof(T) + 2 * NT * sizeof(double);
+  }
+};
+
+// element (row, k) of a k-pair buffer
+template <int RS2>
+__device__ __forceinline__ int kpi(int row, int k) {
+  return (k >> 1) * RS2 + row * 2 + (k & 1);
+}
+
+// acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][8g + j]
+template <typename T, int W, int RPT, int RS2>
+__device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
+                                          T (&acc)[RPT][8]) {
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[r][j] = T(0);
+  const T* ap = A + rg * (2 * RPT);
+  const T* bp = B + 8 * g;
+#pragma unroll 4
+  for (int kp = 0; kp < W / 2; ++kp) {
+    T av[2 * RPT];
+    vload(av, ap + kp * RS2);
+    T b0[8], b1[8];
+    vload(b0, bp + (2 * kp) * W);
+    vload(b1, bp + (2 * kp + 1) * W);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[r][j] = fma(av[2 * r], b0[j], acc[r][j]);
+        acc[r][j] = fma(av[2 * r + 1], b1[j], acc[r][j]);
+      }
+  }
+}
+
+// store a thread's [RPT][8] block (rows rg*RPT.., units 8g..8g+7) into a k-pair buffer
+template <typename T, int RPT, int RS2>
+__device__ __forceinline__ void store_block(T* __restrict__ buf, int rg, int g, const T (&v)[RPT][8]) {
+#pragma unroll
+  for (int jp = 0; jp < 4; ++jp) {
+    T tmp[2 * RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      tmp[2 * r] = v[r][2 * jp];
+      tmp[2 * r + 1] = v[r][2 * jp + 1];
+    }
+    vstore(buf + (4 * g + jp) * RS2 + rg * (2 * RPT), tmp);
+  }
+}
+
+template <typename T, int RPT, int RS2>
+__device__ __forceinline__ void load_block(T (&v)[RPT][8], const T* __restrict__ buf, int rg, int g) {
+#pragma unroll
+  for (int jp = 0; jp < 4; ++jp) {
+    T tmp[2 * RPT];
+    vload(tmp, buf + (4 * g + jp) * RS2 + rg * (2 * RPT));
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      v[r][2 * jp] = tmp[2 * r];
+      v[r][2 * jp + 1] = tmp[2 * r + 1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <typename T, int ACT, int MODE, int REG, int W>
+__global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_kernel(KArgs a) {
+  using C = JetCfg<T, ACT, MODE, REG, W>;
+  constexpr int NT = C::NT, G = C::G, RPT = C::RPT, ROWS = C::ROWS, PPT = C::PPT;
+  constexpr int DIN = C::DIN, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
+  constexpr int NG = C::NG, NL = C::NL, LAP0 = C::LAP0, RS2 = C::RS2;
+  constexpr int NST0 = C::NST0, NSTH = C::NSTH, PP = C::PP;
+  constexpr bool JET = C::JET, BWD = C::BWD;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = a.L;
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* Xs = sm;                      sm += C::al(C::XELEMS);
+  T* Gs = nullptr;
+  if constexpr (BWD) { Gs = sm; sm += C::al(C::XELEMS); }
+  T* slot0 = sm;                   sm += W * W;
+  T* slot1 = sm;                   sm += W * W;
+  T* W0s = sm;                     sm += C::al(DIN * W);
+  T* Bs = sm;                      sm += C::al(L * W);
+  T* WLs = sm;                     sm += C::al(W * NOUT);
+  T* bLs = sm;                     sm += 4;
+  T* Ys = sm;                      sm += C::al(ROWS * NOUT);
+  T* Ybs = nullptr;
+  if constexpr (BWD) { Ybs = sm; sm += C::al(ROWS * NOUT); }
+  T* Ps = sm;                      sm += C::al(PPT * DIN);
+  T* TUs = nullptr;
+  T* TPs = nullptr;
+  if constexpr (MODE == MODE_MSE) {
+    TUs = sm; sm += C::al(PPT * NVEL);
+    TPs = sm; sm += C::al(PPT);
+  }
+  double* red = reinterpret_cast<double*>(sm);
+
+  const int tid = threadIdx.x;
+  const int g = tid % G;
+  const int rg = tid / G;
+  const T* kp = static_cast<const T*>(a.kp);
+  const ParamLayout pl{DIN, W, NOUT, L};
+  const long long n = a.n;
+
+  for (int i = tid; i < DIN * W; i += NT) W0s[i] = kp[pl.off_w(0) + i];
+  for (int i = tid; i < L * W; i += NT) Bs[i] = kp[pl.off_b(i / W) + i % W];
+  for (int i = tid; i < W * NOUT; i += NT) WLs[i] = kp[pl.off_w(L) + i];
+  if (tid < NOUT) bLs[tid] = kp[pl.off_b(L) + tid];
+
+  double* gp = nullptr;
+  if constexpr (BWD) {
+    gp = a.gpart + size_t(blockIdx.x) * a.np_pad;
+    for (int i = tid; i < a.np_pad; i += NT) gp[i] = 0.0;
+  }
+  T* stash = static_cast<T*>(a.scratch) + size_t(blockIdx.x) * a.stash_elems;
+  auto st_idx = [&](int layer, int q) { return (C::stash_layer_base(layer) + q) * NT + tid; };
+
+  double lacc0 = 0.0, lacc1 = 0.0;
+
+  // weight-matrix stream: W_1..W_{L-1} (forward) then W_{L-1}^T..W_1^T (dX)
+  const int nmat = (L - 1) * (BWD ? 2 : 1);
+  auto mat_src = [&](int idx) -> const T* {
+    int i = idx % nmat;
+    if (i < L - 1) return kp + pl.off_w(i + 1);
+    return kp + pl.off_wt(2 * L - 2 - i);
+  };
+  auto stage = [&](int idx) {
+    T* dst = (idx & 1) ? slot1 : slot0;
+    const T* src = mat_src(idx);
+    constexpr int CH = W * W * int(sizeof(T)) / 16;
+    for (int i = tid; i < CH; i += NT)
+      cp_async16(reinterpret_cast<char*>(dst) + 16 * i, reinterpret_cast<const char*>(src) + 16 * i);
+    cp_async_commit();
+  };
+  int ws = 0;
+  if (nmat > 0) {
+    stage(0);
+    cp_async_wait_all();
+  }
+  __syncthreads();
+
+  const long long ntiles = (n + PPT - 1) / PPT;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long p0 = tile * PPT;
+    {
+      const T* pts = static_cast<const T*>(a.pts) + p0 * DIN;
+      const long long rem = n - p0;
+      for (int i = tid; i < PPT * DIN; i += NT) Ps[i] = (i / DIN < rem) ? pts[i] : T(0);
+      if constexpr (MODE == MODE_MSE) {
+        const T* tu = static_cast<const T*>(a.tu) + p0 * NVEL;
+        for (int i = tid; i < PPT * NVEL; i += NT) TUs[i] = (i / NVEL < rem) ? tu[i] : T(0);
+        if (a.has_p) {
+          const T* tpp = static_cast<const T*>(a.tp) + p0;
+          for (int i = tid; i < PPT; i += NT) TPs[i] = (i < rem) ? tpp[i] : T(0);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- layer 0 (DIN -> W): derivative blocks are constant ----------------
+    {
+      T outv[RPT][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int u = 8 * g + j;
+        const T b0 = Bs[u];
+#pragma unroll
+        for (int pr = 0; pr < PP; ++pr) {
+          const int pt = JET ? rg : rg * RPT + pr;
+          T zv = T(0);
+#pragma unroll
+          for (int i = 0; i < DIN; ++i) zv = fma(Ps[pt * DIN + i], W0s[i * W + u], zv);
+          zv += b0;
+          T s, c;
+          act_eval<ACT>(zv, s, c);
+          if constexpr (JET) {
+            T d1, d2;
+            act_d12<ACT>(s, c, d1, d2);
+            outv[0][j] = s;
+#pragma unroll
+            for (int i = 0; i < NG; ++i) outv[1 + i][j] = d1 * W0s[i * W + u];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+              const T zg = W0s[(LAP0 + i) * W + u];
+              outv[1 + NG + i][j] = d2 * zg * zg;
+            }
+          } else {
+            outv[pr][j] = s;
+          }
+          if constexpr (BWD) {
+            stash[st_idx(0, (pr * 8 + j) * NST0)] = s;
+            if constexpr (C::SIN) stash[st_idx(0, (pr * 8 + j) * NST0 + 1)] = c;
+          }
+        }
+      }
+      store_block<T, RPT, RS2>(Xs, rg, g, outv);
+    }
+    __syncthreads();
+
+    // ---------------- hidden layers 1..L-1 ----------------
+    for (int l = 1; l < L; ++l) {
+      const T* Bm = (ws & 1) ? slot1 : slot0;
+      stage(ws + 1);
+      T acc[RPT][8];
+      gemm_rows<T, W, RPT, RS2>(Xs, Bm, rg, g, acc);
+      __syncthreads();
+      T outv[RPT][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int u = 8 * g + j;
+        const T bl = Bs[l * W + u];
+        if constexpr (JET) {
+          const T zv = acc[0][j] + bl;
+          T s, c, d1, d2;
+          act_eval<ACT>(zv, s, c);
+          act_d12<ACT>(s, c, d1, d2);
+          outv[0][j] = s;
+#pragma unroll
+          for (int i = 0; i < NG; ++i) outv[1 + i][j] = d1 * acc[1 + i][j];
+#pragma unroll
+          for (int i = 0; i < NL; ++i) {
+            const T zg = acc[1 + LAP0 + i][j];
+            outv[1 + NG + i][j] = d2 * zg * zg + d1 * acc[1 + NG + i][j];
+          }
+          if constexpr (BWD) {
+            const int q = j * NSTH;
+            stash[st_idx(l, q)] = s;
+            if constexpr (C::SIN) stash[st_idx(l, q + 1)] = c;
+#pragma unroll
+            for (int i = 0; i < NG; ++i) stash[st_idx(l, q + 1 + C::SIN + i)] = acc[1 + i][j];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) stash[st_idx(l, q + 1 + C::SIN + NG + i)] = acc[1 + NG + i][j];
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const T zv = acc[r][j] + bl;
+            T s, c;
+            act_eval<ACT>(zv, s, c);
+            outv[r][j] = s;
+            if constexpr (BWD) {
+              stash[st_idx(l, (r * 8 + j) * NST0)] = s;
+              if constexpr (C::SIN) stash[st_idx(l, (r * 8 + j) * NST0 + 1)] = c;
+            }
+          }
+        }
+      }
+      store_block<T, RPT, RS2>(Xs, rg, g, outv);
+      cp_async_wait_all();
+      __syncthreads();
+      ++ws;
+    }
+
+    // ---------------- output layer (W -> NOUT) ----------------
+    for (int r = tid; r < ROWS; r += NT) {
+      T y[NOUT];
+#pragma unroll
+      for (int c = 0; c < NOUT; ++c) y[c] = T(0);
+#pragma unroll 8
+      for (int kp2 = 0; kp2 < W / 2; ++kp2) {
+        T xv[2];
+        vload(xv, Xs + kp2 * RS2 + r * 2);
+#pragma unroll
+        for (int c = 0; c < NOUT; ++c) {
+          y[c] = fma(xv[0], WLs[(2 * kp2) * NOUT + c], y[c]);
+          y[c] = fma(xv[1], WLs[(2 * kp2 + 1) * NOUT + c], y[c]);
+        }
+      }
+      const bool vrow = JET ? (r % S == 0) : true;
+#pragma unroll
+      for (int c = 0; c < NOUT; ++c) Ys[r * NOUT + c] = vrow ? y[c] + bLs[c] : y[c];
+    }
+    __syncthreads();
+
+    // ---------------- head ----------------
+    const long long rem = n - p0;
+    if constexpr (MODE == MODE_VALUE) {
+      T* out = static_cast<T*>(a.out) + p0 * NOUT;
+      for (int i = tid; i < PPT * NOUT; i += NT)
+        if (i / NOUT < rem) out[i] = Ys[i];
+      __syncthreads();
+      continue;
+    } else if constexpr (MODE == MODE_JET) {
+      T* out = static_cast<T*>(a.out) + p0 * S * NOUT;
+      for (int i = tid; i < PPT * S * NOUT; i += NT)
+        if (i / (S * NOUT) < rem) out[i] = Ys[i];
+      __syncthreads();
+      continue;
+    } else if constexpr (MODE == MODE_PDE) {
+      // Navier-Stokes residual head (physics.py:70-93; builders.py:51-64, :98-99)
+      using R = Regime<REG>;
+      constexpr int NSP = R::NSP, TOFF = R::HAS_T;
+      const T inv_re = T(a.inv_re);
+      const T two_coef = T(2.0 * a.coef);
+      for (int pt = tid; pt < PPT; pt += NT) {
+        const T* y = Ys + pt * S * NOUT;
+        T* yb = Ybs + pt * S * NOUT;
+#pragma unroll
+        for (int i = 0; i < S * NOUT; ++i) yb[i] = T(0);
+        if (pt >= rem) continue;
+        auto Y = [&](int s, int c) { return y[s * NOUT + c]; };
+        auto GRAD = [&](int in) { return 1 + in; };
+        auto LAP = [&](int in) { return 1 + NG + (in - LAP0); };
+        constexpr int P = NVEL;  // pressure channel
+        T r[NVEL + 1];
+#pragma unroll
+        for (int i = 0; i < NVEL; ++i) {
+          const int xi = TOFF + i;
+          T acc = T(0);
+          if constexpr (R::HAS_T) acc = Y(GRAD(0), i);
+          acc = (R::HAS_T ? acc + Y(GRAD(xi), P) : Y(GRAD(xi), P));
+#pragma unroll
+          for (int jj = 0; jj < NSP; ++jj) acc += -inv_re * Y(LAP(TOFF + jj), i);
+#pragma unroll
+          for (int k = 0; k < NVEL; ++k) acc += Y(0, k) * Y(GRAD(TOFF + k), i);
+          r[i] = acc;
+        }
+        {
+          T acc = Y(GRAD(TOFF), 0);
+#pragma unroll
+          for (int k = 1; k < NVEL; ++k) acc += Y(GRAD(TOFF + k), k);
+          r[NVEL] = acc;
+        }
+        double sq = 0.0;
+#pragma unroll
+        for (int i = 0; i <= NVEL; ++i) sq += double(r[i]) * double(r[i]);
+        lacc0 += sq;
+        // adjoints of the jet outputs
+#pragma unroll
+        for (int i = 0; i < NVEL; ++i) {
+          const T rb = two_coef * r[i];
+          const int xi = TOFF + i;
+          if constexpr (R::HAS_T) yb[GRAD(0) * NOUT + i] += rb;
+          yb[GRAD(xi) * NOUT + P] += rb;
+#pragma unroll
+          for (int jj = 0; jj < NSP; ++jj) yb[LAP(TOFF + jj) * NOUT + i] += -inv_re * rb;
+#pragma unroll
+          for (int k = 0; k < NVEL; ++k) {
+            yb[0 * NOUT + k] += rb * Y(GRAD(TOFF + k), i);
+            yb[GRAD(TOFF + k) * NOUT + i] += rb * Y(0, k);
+          }
+        }
+        {
+          const T rb = two_coef * r[NVEL];
+#pragma unroll
+          for (int k = 0; k < NVEL; ++k) yb[GRAD(TOFF + k) * NOUT + k] += rb;
+        }
+      }
+    } else {  // MODE_MSE: squared error against targets (builders.py:103-141)
+      const T two_vc = T(2.0 * a.coef);
+      const T two_pc = T(2.0 * a.pcoef);
+      for (int pt = tid; pt < PPT; pt += NT) {
+        T* yb = Ybs + pt * NOUT;
+#pragma unroll
+        for (int c = 0; c < NOUT; ++c) yb[c] = T(0);
+        if (pt >= rem) continue;
+        const T* y = Ys + pt * NOUT;
+        double squ = 0.0;
+#pragma unroll
+        for (int c = 0; c < NVEL; ++c) {
+          const T d = y[c] - TUs[pt * NVEL + c];
+          const T w = T(a.velw[c]);
+          squ += double(a.velw[c]) * (double(d) * double(d));
+          yb[c] = (two_vc * w) * d;
+        }
+        lacc0 += squ;
+        if (a.has_p) {
+          const T d = y[NVEL] - TPs[pt];
+          lacc1 += double(d) * double(d);
+          yb[NVEL] = two_pc * d;
+        }
+      }
+    }
+    __syncthreads();
+
+    if constexpr (BWD) {
+      // ---------------- output layer backward ----------------
+      for (int i = tid; i < W * NOUT; i += NT) {
+        const int k = i / NOUT, c = i % NOUT;
+        T s = T(0);
+        for (int r = 0; r < ROWS; ++r) s = fma(Xs[kpi<RS2>(r, k)], Ybs[r * NOUT + c], s);
+        gp[pl.off_w(L) + i] += double(s);
+      }
+      if (tid < NOUT) {
+        T s = T(0);
+        for (int pt = 0; pt < PPT; ++pt) s += Ybs[(JET ? pt * S : pt) * NOUT + tid];
+        gp[pl.off_b(L) + tid] += double(s);
+      }
+      {
+        T gv[RPT][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int u = 8 * g + j;
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int row = rg * RPT + r;
+            T s = T(0);
+#pragma unroll
+            for (int c = 0; c < NOUT; ++c) s = fma(Ybs[row * NOUT + c], WLs[u * NOUT + c], s);
+            gv[r][j] = s;
+          }
+        }
+        store_block<T, RPT, RS2>(Gs, rg, g, gv);
+      }
+      __syncthreads();
+
+      // ---------------- hidden layers L-1..1 ----------------
+      for (int l = L - 1; l >= 1; --l) {
+        // activation backward (numpy_backend.py:58-89): S-bar -> Z-bar, in place in Gs
+        {
+          T sb[RPT][8];
+          load_block<T, RPT, RS2>(sb, Gs, rg, g);
+          T zb[RPT][8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if constexpr (JET) {
+              const int q = j * NSTH;
+              const T s = stash[st_idx(l, q)];
+              const T c = C::SIN ? stash[st_idx(l, q + 1)] : T(0);
+              T zg[NG], zl[NL > 0 ? NL : 1];
+#pragma unroll
+              for (int i = 0; i < NG; ++i) zg[i] = stash[st_idx(l, q + 1 + C::SIN + i)];
+#pragma unroll
+              for (int i = 0; i < NL; ++i) zl[i] = stash[st_idx(l, q + 1 + C::SIN + NG + i)];
+              T d1, d2;
+              act_d12<ACT>(s, c, d1, d2);
+              const T d3 = act_d3<ACT>(s, c, d1, d2);
+              T zv = sb[0][j] * d1;
+#pragma unroll
+              for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * (d2 * zg[i]);
+#pragma unroll
+              for (int i = 0; i < NL; ++i) {
+                const T gg = zg[LAP0 + i];
+                zv += sb[1 + NG + i][j] * (d3 * gg * gg + d2 * zl[i]);
+              }
+              zb[0][j] = zv;
+#pragma unroll
+              for (int i = 0; i < NG; ++i) {
+                T t = sb[1 + i][j] * d1;
+                if (i >= LAP0) t += (T(2) * d2) * zg[i] * sb[1 + NG + (i - LAP0)][j];
+                zb[1 + i][j] = t;
+              }
+#pragma unroll
+              for (int i = 0; i < NL; ++i) zb[1 + NG + i][j] = sb[1 + NG + i][j] * d1;
+            } else {
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) {
+                const T s = stash[st_idx(l, (r * 8 + j) * NST0)];
+                const T c = C::SIN ? stash[st_idx(l, (r * 8 + j) * NST0 + 1)] : T(0);
+                T d1, d2;
+                act_d12<ACT>(s, c, d1, d2);
+                zb[r][j] = sb[r][j] * d1;
+              }
+            }
+          }
+          store_block<T, RPT, RS2>(Gs, rg, g, zb);
+        }
+        // rebuild this layer's input H_l = jets of layer l-1 into Xs
+        {
+          T hv[RPT][8];
+          const int lp = l - 1;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int u = 8 * g + j;
+            if constexpr (JET) {
+              const int nst = lp == 0 ? NST0 : NSTH;
+              const int q = j * nst;
+              const T s = stash[st_idx(lp, q)];
+              const T c = C::SIN ? stash[st_idx(lp, q + 1)] : T(0);
+              T d1, d2;
+              act_d12<ACT>(s, c, d1, d2);
+              hv[0][j] = s;
+              if (lp == 0) {
+#pragma unroll
+                for (int i = 0; i < NG; ++i) hv[1 + i][j] = d1 * W0s[i * W + u];
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                  const T zg = W0s[(LAP0 + i) * W + u];
+                  hv[1 + NG + i][j] = d2 * zg * zg;
+                }
+              } else {
+                T zg[NG];
+#pragma unroll
+                for (int i = 0; i < NG; ++i) {
+                  zg[i] = stash[st_idx(lp, q + 1 + C::SIN + i)];
+                  hv[1 + i][j] = d1 * zg[i];
+                }
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                  const T zl = stash[st_idx(lp, q + 1 + C::SIN + NG + i)];
+                  const T gg = zg[LAP0 + i];
+                  hv[1 + NG + i][j] = d2 * gg * gg + d1 * zl;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) hv[r][j] = stash[st_idx(lp, (r * 8 + j) * NST0)];
+            }
+          }
+          store_block<T, RPT, RS2>(Xs, rg, g, hv);
+        }
+        __syncthreads();
+        stage(ws + 1);
+
+        // dW_l = H_l^T Zbar_l over all rows of the tile (thread tile 4k x 4u)
+        {
+          constexpr int Q = W / 4;
+          for (int t = tid; t < Q * Q; t += NT) {
+            const int kq = t % Q, uq = t / Q;
+            T acc[4][4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
+            const T* x0p = Xs + kq * RS2;
+            const T* x1p = Xs + (kq + Q) * RS2;
+            const T* z0p = Gs + uq * RS2;
+            const T* z1p = Gs + (uq + Q) * RS2;
+#pragma unroll 4
+            for (int r = 0; r < ROWS; r += 2) {
+              T x0[4], x1[4], z0[4], z1[4];
+              vload(x0, x0p + 2 * r);
+              vload(x1, x1p + 2 * r);
+              vload(z0, z0p + 2 * r);
+              vload(z1, z1p + 2 * r);
+#pragma unroll
+              for (int rr = 0; rr < 2; ++rr) {
+                const T hk[4] = {x0[2 * rr], x0[2 * rr + 1], x1[2 * rr], x1[2 * rr + 1]};
+                const T zu[4] = {z0[2 * rr], z0[2 * rr + 1], z1[2 * rr], z1[2 * rr + 1]};
+#pragma unroll
+                for (int x = 0; x < 4; ++x)
+#pragma unroll
+                  for (int y = 0; y < 4; ++y) acc[x][y] = fma(hk[x], zu[y], acc[x][y]);
+              }
+            }
+            const int kk[4] = {2 * kq, 2 * kq + 1, 2 * (kq + Q), 2 * (kq + Q) + 1};
+            const int uu[4] = {2 * uq, 2 * uq + 1, 2 * (uq + Q), 2 * (uq + Q) + 1};
+            const int base = pl.off_w(l);
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) gp[base + kk[x] * W + uu[y]] += double(acc[x][y]);
+          }
+          if (tid < W) {
+            T s = T(0);
+            for (int pt = 0; pt < PPT; ++pt) s += Gs[kpi<RS2>(JET ? pt * S : pt, tid)];
+            gp[pl.off_b(l) + tid] += double(s);
+          }
+        }
+        // dX: S-bar_{l-1} = Zbar_l W_l^T
+        {
+          const T* Bm = (ws & 1) ? slot1 : slot0;
+          T acc[RPT][8];
+          gemm_rows<T, W, RPT, RS2>(Gs, Bm, rg, g, acc);
+          __syncthreads();
+          store_block<T, RPT, RS2>(Gs, rg, g, acc);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        ++ws;
+      }
+
+      // ---------------- layer 0 backward ----------------
+      {
+        T sb[RPT][8];
+        load_block<T, RPT, RS2>(sb, Gs, rg, g);
+        T zb[RPT][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int u = 8 * g + j;
+          if constexpr (JET) {
+            const T s = stash[st_idx(0, j * NST0)];
+            const T c = C::SIN ? stash[st_idx(0, j * NST0 + 1)] : T(0);
+            T d1, d2;
+            act_d12<ACT>(s, c, d1, d2);
+            const T d3 = act_d3<ACT>(s, c, d1, d2);
+            T zg[NG];
+#pragma unroll
+            for (int i = 0; i < NG; ++i) zg[i] = W0s[i * W + u];
+            T zv = sb[0][j] * d1;
+#pragma unroll
+            for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * (d2 * zg[i]);
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+              const T gg = zg[LAP0 + i];
+              zv += sb[1 + NG + i][j] * (d3 * gg * gg);
+            }
+            zb[0][j] = zv;
+#pragma unroll
+            for (int i = 0; i < NG; ++i) {
+              T t = sb[1 + i][j] * d1;
+              if (i >= LAP0) t += (T(2) * d2) * zg[i] * sb[1 + NG + (i - LAP0)][j];
+              zb[1 + i][j] = t;
+            }
+#pragma unroll
+            for (int i = 0; i < NL; ++i) zb[1 + NG + i][j] = sb[1 + NG + i][j] * d1;
+          } else {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+              const T s = stash[st_idx(0, (r * 8 + j) * NST0)];
+              const T c = C::SIN ? stash[st_idx(0, (r * 8 + j) * NST0 + 1)] : T(0);
+              T d1, d2;
+              act_d12<ACT>(s, c, d1, d2);
+              zb[r][j] = sb[r][j] * d1;
+            }
+          }
+        }
+        store_block<T, RPT, RS2>(Gs, rg, g, zb);
+      }
+      __syncthreads();
+      // dW0 = X^T Zbar over the stacked input (value rows hold the points, the
+      // derivative block j is the unit vector e_j, tape.py:426-436); db0.
+      for (int i = tid; i < (DIN + 1) * W; i += NT) {
+        const int j = i / W, u = i % W;
+        T s = T(0);
+        if (j < DIN) {
+          for (int pt = 0; pt < PPT; ++pt) {
+            const int row = JET ? pt * S : pt;
+            s = fma(Ps[pt * DIN + j], Gs[kpi<RS2>(row, u)], s);
+            if constexpr (JET) s += Gs[kpi<RS2>(row + 1 + j, u)];
+          }
+          gp[pl.off_w(0) + j * W + u] += double(s);
+        } else {
+          for (int pt = 0; pt < PPT; ++pt) s += Gs[kpi<RS2>(JET ? pt * S : pt, u)];
+          gp[pl.off_b(0) + u] += double(s);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  if constexpr (BWD) {
+    cp_async_wait_all();
+    red[tid] = lacc0;
+    red[NT + tid] = lacc1;
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int i = 0; i < NT; ++i) {
+        s0 += red[i];
+        s1 += red[NT + i];
+      }
+      a.lpart[2 * blockIdx.x] = s0;
+      a.lpart[2 * blockIdx.x + 1] = s1;
+    }
+  }
+}
+
+}  // namespace fr

@@ -1,0 +1,354 @@
+"""Training driver: plan assembly and the GPU epoch loops.
+
+Mirrors pkg/src/flowrec/runtime/driver.py:43-283.  Backends:
+
+  "serial" / "cuda"  every rank in this process on the current GPU (the
+                     reference's serial backend, :127-144).  The exchange is
+                     device-to-device: each producer packs straight into its
+                     destination's ghost-target rows.  After an eager first
+                     epoch the loop is replayed from CUDA graphs (one with the
+                     exchange, one without), so an epoch costs one graph launch.
+  "distributed"      this process is one rank of an initialised
+                     torch.distributed group (one process per GPU, launched by
+                     torchrun); ghost messages move by NCCL point-to-point,
+                     overlapped with the interior (obs + PDE) kernels.
+  "process"          spawns one process per rank, one GPU each (needs at least
+                     as many GPUs as ranks) and runs "distributed" in each.
+
+Semantics kept: the exchange happens before the step of epoch e with the
+parameters after epoch e-1, including e = 0 (:133-142); history rows are the
+pre-update unweighted parts; masters normalise every outgoing pressure.
+"""
+
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ..decomposition import identify_masters
+from ..network import ExpertConfig, ExpertParams
+from ..physics import FlowRegime
+from .worker import OutgoingEdge, RankWorker, TrainConfig, WorkerSpec, derive_param_seed
+
+
+class DeadlockError(RuntimeError):
+    pass
+
+
+class RankFailure(RuntimeError):
+    pass
+
+
+@dataclass(frozen=True)
+class TrainingPlan:
+    regime: FlowRegime
+    subdomains: tuple
+    masters: frozenset
+    expert_config: ExpertConfig
+    train_config: TrainConfig
+    worker_specs: tuple
+
+    @property
+    def n_ranks(self):
+        return len(self.worker_specs)
+
+
+@dataclass
+class TrainResult:
+    params: dict
+    history: dict
+    epoch_times: dict
+    exchange_log: dict
+    wall_time_s: float = 0.0
+
+    def median_epoch_time(self):
+        """Median over epochs of the slowest rank's epoch duration (:65-68)."""
+        stacked = np.stack([self.epoch_times[r] for r in sorted(self.epoch_times)])
+        return float(np.median(np.max(stacked, axis=0)))
+
+
+def build_plan(subdomains, datasets, expert_config: ExpertConfig, train_config: TrainConfig) -> TrainingPlan:
+    """Roles, effective weights and message routes (driver.py:71-121)."""
+    regime = subdomains[0].domain.regime
+    anchored = train_config.pressure_coupling == "anchored_master"
+    masters = identify_masters(subdomains, train_config.anchor)
+    if anchored and subdomains[0].time_splits > 1 and not train_config.weights.ghost_p_time > 0:
+        raise ValueError("temporal ghost pressure weight must be positive when the domain is split in time")
+    outgoing = {s.rank_index: [] for s in subdomains}
+    for s in subdomains:
+        ds = datasets[s.rank_index]
+        if len(ds.ghosts) != len(s.ghosts):
+            raise ValueError(f"rank {s.rank_index}: datasets do not match the partition")
+        for gi, g in enumerate(ds.ghosts):
+            outgoing[g.neighbor].append(OutgoingEdge(s.rank_index, gi, g.kind, g.points))
+    specs = []
+    for s in subdomains:
+        master = anchored and s.rank_index in masters
+        w = train_config.weights.as_master() if master else train_config.weights
+        specs.append(WorkerSpec(
+            rank=s.rank_index, role="master" if master else "slave", spec=s, regime=regime,
+            expert_config=expert_config, train_config=train_config, datasets=datasets[s.rank_index],
+            effective_weights=w, outgoing=tuple(outgoing[s.rank_index]),
+            param_seed=derive_param_seed(train_config.seed, s.rank_index), normalize_outgoing=master,
+        ))
+    return TrainingPlan(regime, tuple(subdomains), masters, expert_config, train_config, tuple(specs))
+
+
+# -- in-process (single GPU, all ranks) ---------------------------------------------
+
+
+class LocalTrainer:
+    """All ranks of a plan resident on one GPU with a device-to-device exchange."""
+
+    def __init__(self, plan: TrainingPlan, dtype="float32", epochs=None):
+        self.plan = plan
+        self.workers = {ws.rank: RankWorker(ws, dtype=dtype, epochs=epochs) for ws in plan.worker_specs}
+        self.order = sorted(self.workers)
+        self.routes = []
+        for r in self.order:
+            w = self.workers[r]
+            for k, (edge, _, _, _) in enumerate(w.edges):
+                tu, tp = self.workers[edge.dest].objective.target_slice(edge.ghost_index)
+                self.routes.append((w, k, tu, tp))
+        self.graphs = {}
+        self._ran_eager = False
+
+    def enqueue_exchange(self):
+        for r in self.order:
+            self.workers[r].produce()
+        for w, k, tu, tp in self.routes:
+            w.pack_edge(k, tu, tp)
+        for w in self.workers.values():
+            w.objective.mark_targets_set()
+
+    def enqueue_step(self):
+        for r in self.order:
+            self.workers[r].enqueue_epoch()
+
+    def _enqueue(self, exchange):
+        if exchange:
+            self.enqueue_exchange()
+        self.enqueue_step()
+
+    def _graph(self, exchange):
+        g = self.graphs.get(exchange)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._enqueue(exchange)
+            self.graphs[exchange] = g
+        return g
+
+    def check_flags(self):
+        for w in self.workers.values():
+            w.check_flags()
+
+    def log_exchange(self, e):
+        for w in self.workers.values():
+            w.exchange_log.append((e, sorted(w.expected_messages)))
+
+    def run(self, epochs, start=0, use_graphs=True, record_times=True):
+        """Train `epochs` epochs; returns per-epoch device times (s)."""
+        comm = self.plan.train_config.comm_interval
+        events = []
+        for i, e in enumerate(range(start, start + epochs)):
+            exchange = e % comm == 0
+            if record_times:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                events.append(ev)
+            # the trainer's first epoch runs eagerly (it also initialises every
+            # lazily set attribute); later epochs replay captured graphs of the
+            # same work
+            if use_graphs and self._ran_eager:
+                self._graph(exchange).replay()
+            else:
+                self._enqueue(exchange)
+                self._ran_eager = True
+            if exchange:
+                self.log_exchange(e)
+            for w in self.workers.values():
+                w.epochs_done += 1
+        if not record_times:
+            return None  # asynchronous: caller synchronises and calls check_flags()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        events.append(ev)
+        torch.cuda.synchronize()
+        self.check_flags()
+        times = np.array([a.elapsed_time(b) * 1e-3 for a, b in zip(events[:-1], events[1:])])
+        for w in self.workers.values():
+            w.epoch_times.extend(times.tolist())
+        return times
+
+
+def _train_local(plan, dtype, use_graphs):
+    t0 = time.perf_counter()
+    trainer = LocalTrainer(plan, dtype=dtype)
+    trainer.run(plan.train_config.epochs, use_graphs=use_graphs)
+    return _collect(plan, {r: w.export() for r, w in trainer.workers.items()}, time.perf_counter() - t0)
+
+
+# -- one process per GPU -------------------------------------------------------------
+
+
+def p2p_routes(plan: TrainingPlan, rank: int):
+    """(sends, recvs) of one rank: sends [(dest, edge_index, n)], recvs
+    [(source, ghost_index, n)], both sorted by (peer, ghost index) (:83-91)."""
+    ws = plan.worker_specs[rank]
+    sends = [(e.dest, k, e.points.shape[0]) for k, e in enumerate(ws.outgoing)]
+    recvs = [(g.neighbor, gi, g.points.shape[0]) for gi, g in enumerate(ws.datasets.ghosts)]
+    return sends, recvs
+
+
+def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
+    """Issue every send/recv of one round as a single batched P2P group.
+
+    send_bufs[k] / recv_bufs[gi] are (u, p) tensor pairs.  Returns the work
+    handles; waiting on them orders the caller's stream after the transfers."""
+    import torch.distributed as dist
+
+    ops = []
+    for dest, k, _ in sends:
+        u, p = send_bufs[k]
+        ops += [dist.P2POp(dist.isend, u, dest, group), dist.P2POp(dist.isend, p, dest, group)]
+    for src, gi, _ in recvs:
+        u, p = recv_bufs[gi]
+        ops += [dist.P2POp(dist.irecv, u, src, group), dist.P2POp(dist.irecv, p, src, group)]
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+class DistributedTrainer:
+    """This process's rank of a torch.distributed group (NCCL over NVLink)."""
+
+    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None):
+        import torch.distributed as dist
+
+        self.plan = plan
+        self.rank = dist.get_rank() if rank is None else rank
+        if dist.get_world_size() != plan.n_ranks:
+            raise ValueError(f"world size {dist.get_world_size()} != plan ranks {plan.n_ranks}")
+        self.worker = w = RankWorker(plan.worker_specs[self.rank], dtype=dtype, epochs=epochs)
+        self.sends, self.recvs = p2p_routes(plan, self.rank)
+        nv, T, dev = plan.regime.n_vel, w.plan.tdtype, w.plan.device
+        self.send_bufs = [(torch.empty((n, nv), dtype=T, device=dev), torch.empty(n, dtype=T, device=dev))
+                          for _, _, n in self.sends]
+        self.recv_bufs = {gi: w.objective.target_slice(gi) for _, gi, _ in self.recvs}
+
+    def epoch(self, e):
+        w = self.worker
+        exchange = e % self.plan.train_config.comm_interval == 0
+        works = []
+        if exchange:
+            w.produce()
+            for k, _ in enumerate(self.sends):
+                w.pack_edge(k, *self.send_bufs[k])
+            works = post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs)
+            w.objective.mark_targets_set()
+        w.enqueue_epoch(part="interior")   # overlaps the NCCL transfers
+        for wk in works:
+            wk.wait()                      # compute stream waits for the receives
+        w.enqueue_epoch(part="rest")
+        w.epochs_done += 1
+        if exchange:
+            w.exchange_log.append((e, sorted(w.expected_messages)))
+
+    def run(self, epochs, start=0):
+        events = []
+        for e in range(start, start + epochs):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            events.append(ev)
+            self.epoch(e)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        events.append(ev)
+        torch.cuda.synchronize()
+        self.worker.check_flags()
+        times = [a.elapsed_time(b) * 1e-3 for a, b in zip(events[:-1], events[1:])]
+        self.worker.epoch_times.extend(times)
+        return times
+
+
+def _train_distributed(plan, dtype):
+    import torch.distributed as dist
+
+    t0 = time.perf_counter()
+    tr = DistributedTrainer(plan, dtype=dtype)
+    tr.run(plan.train_config.epochs)
+    exports = [None] * plan.n_ranks
+    dist.all_gather_object(exports, (tr.rank, tr.worker.export()))
+    return _collect(plan, dict(exports), time.perf_counter() - t0)
+
+
+def _process_entry(local_rank, plan, dtype, port, q):
+    import torch.distributed as dist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", rank=local_rank, world_size=plan.n_ranks)
+        res = _train_distributed(plan, dtype)
+        if local_rank == 0:
+            q.put(("ok", res))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+
+        q.put(("error", f"rank {local_rank}:\n{traceback.format_exc()}"))
+
+
+def _train_process(plan, dtype, timeout):
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < plan.n_ranks:
+        raise RankFailure(f"backend 'process' needs {plan.n_ranks} GPUs, found {torch.cuda.device_count()}")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_process_entry, args=(r, plan, dtype, port, q), daemon=True)
+             for r in range(plan.n_ranks)]
+    for p in procs:
+        p.start()
+    try:
+        status, payload = q.get(timeout=max(timeout, 60.0) * 4)
+    except Exception:
+        status, payload = "error", "coordinator timed out waiting for rank results"
+    finally:
+        for p in procs:
+            p.join(timeout=30.0)
+            if p.is_alive():
+                p.terminate()
+    if status != "ok":
+        raise RankFailure(f"training aborted:\n{payload}")
+    return payload
+
+
+def _collect(plan, exports, wall):
+    params, history, times, xlog = {}, {}, {}, {}
+    for ws in plan.worker_specs:
+        ex = exports[ws.rank]
+        params[ws.rank] = ExpertParams(plan.expert_config, np.asarray(ex["flat"]), seed=ex["param_seed"])
+        history[ws.rank] = np.asarray(ex["history"])
+        times[ws.rank] = np.asarray(ex["epoch_times"])
+        xlog[ws.rank] = ex["exchange_log"]
+    return TrainResult(params, history, times, xlog, wall_time_s=wall)
+
+
+def train(plan: TrainingPlan, backend="serial", exchange_timeout=600.0, dtype="float32", use_graphs=True):
+    """Run the distributed training loop on the GPU(s)."""
+    if backend in ("serial", "cuda"):
+        return _train_local(plan, dtype, use_graphs)
+    if backend == "distributed":
+        return _train_distributed(plan, dtype)
+    if backend == "process":
+        return _train_process(plan, dtype, exchange_timeout)
+    raise ValueError(f"unknown backend {backend!r} (use 'serial', 'cuda', 'distributed' or 'process')")
+
+
+def train_many(plans, n_workers=1, backend="serial", exchange_timeout=600.0, dtype="float32"):
+    """Independent plans (e.g. one per seed): replicas, run one after another."""
+    return [train(p, backend=backend, exchange_timeout=exchange_timeout, dtype=dtype) for p in plans]

@@ -1,0 +1,228 @@
+"""Per-rank composite objective on the GPU.
+
+`DeviceObjective` is the resident form used by the training loop: datasets
+live in HBM, one epoch is a fixed sequence of kernel launches (obs MSE -> PDE
+-> ghost-spatial MSE -> ghost-temporal MSE -> fixed-order reductions), with no
+host synchronisation, so it can be captured in a CUDA graph.
+
+`LocalObjective` keeps the reference's API (pkg/src/flowrec/runtime/objective.py:67-199):
+the same coefficients (lambda/N folded into each loss head, ghost-u normalised
+over the union of ghost kinds, ghost-p per kind, :96-140), the same unweighted
+`LossParts` and the same non-finite guard.  Mini-batching in the reference is
+pure gradient accumulation (:46-64); the GPU processes every point of a
+dataset in one persistent launch, so `batch_size` only validates.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from .. import _lib as X
+from ..engine import get_plan, new_kparams, prepare, to_device
+from ..physics import LossParts, compose_loss
+
+SEG_OBS, SEG_PDE, SEG_GS, SEG_GT = 0, 1, 2, 3
+KINDS = ("spatial", "temporal")
+
+
+class DeviceObjective:
+    """Resident datasets, workspaces and the per-epoch launch sequence."""
+
+    def __init__(self, plan, regime, datasets, weights):
+        self.plan = plan
+        self.regime = regime
+        self.weights = weights
+        dev, T = plan.device, plan.tdtype
+        nv = regime.n_vel
+        self.n_obs = datasets.n_obs
+        self.n_colloc = datasets.n_colloc
+        if self.n_obs == 0 and weights.obs > 0:
+            raise ValueError("observation dataset is empty but the observation weight is positive")
+        if self.n_colloc == 0:
+            raise ValueError("collocation dataset is empty")
+        vw = weights.velocity if weights.velocity is not None else (1.0,) * nv
+        if len(vw) != nv:
+            raise ValueError(f"need one velocity weight per component ({nv}), got {len(vw)}")
+        self.vel_w = (ctypes.c_double * 4)(*(list(vw) + [1.0] * (4 - nv)))
+
+        self.obs_pts = to_device(datasets.obs_points.reshape(-1, regime.n_inputs), T, dev)
+        self.obs_vel = to_device(datasets.obs_velocity.reshape(-1, nv), T, dev)
+        self.col_pts = to_device(datasets.colloc_points, T, dev)
+
+        # ghost sets grouped per kind in ghost-index order (objective.py:115-141)
+        self.ghost_slices = {}  # ghost index -> (kind, offset, n)
+        self.ghost = {}
+        counts = {k: 0 for k in KINDS}
+        per_kind = {k: [] for k in KINDS}
+        for gi, g in enumerate(datasets.ghosts):
+            n = g.points.shape[0]
+            self.ghost_slices[gi] = (g.kind, counts[g.kind], n)
+            counts[g.kind] += n
+            per_kind[g.kind].append(g.points)
+        self.n_ghost = counts
+        self.n_ghost_total = counts["spatial"] + counts["temporal"]
+        for kind in KINDS:
+            if counts[kind] == 0:
+                continue
+            p_w = weights.ghost_p_space if kind == "spatial" else weights.ghost_p_time
+            self.ghost[kind] = {
+                "pts": to_device(np.vstack(per_kind[kind]), T, dev),
+                "tu": torch.zeros((counts[kind], nv), dtype=T, device=dev),
+                "tp": torch.zeros(counts[kind], dtype=T, device=dev),
+                "vel_coef": weights.ghost_u / self.n_ghost_total,
+                "p_coef": p_w / counts[kind],
+            }
+        self.targets_set = {k: False for k in self.ghost}
+
+        # launch list and workspaces: gradient / loss partial rows are laid out
+        # contiguously in dataset order so one fixed-order reduction covers all
+        self.segments = []
+        rows = 0
+        scratch = 0
+        seg_rows = [0, 0, 0, 0]
+        plan_segs = [(SEG_OBS, X.MODE_MSE, self.n_obs), (SEG_PDE, X.MODE_PDE, self.n_colloc)]
+        plan_segs += [(SEG_GS if k == "spatial" else SEG_GT, X.MODE_MSE, counts[k]) for k in KINDS]
+        for seg, mode, n in plan_segs:
+            if n == 0:
+                continue
+            ws = plan.workspace(mode, n)
+            self.segments.append((seg, mode, n, rows, ws))
+            seg_rows[seg] = ws.grid
+            rows += ws.grid
+            scratch = max(scratch, ws.scratch_bytes)
+        self.total_rows = rows
+        self.seg_rows = (ctypes.c_int * 4)(*seg_rows)
+        npad = plan.info.np_pad
+        self.gpart = torch.empty(max(rows, 1) * npad, dtype=torch.float64, device=dev)
+        self.lpart = torch.empty(max(rows, 1) * 2, dtype=torch.float64, device=dev)
+        self.scratch = torch.empty(max(scratch, 16), dtype=torch.uint8, device=dev)
+        self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
+        self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+
+    # -- ghost targets --------------------------------------------------------
+    def target_slice(self, gi):
+        """Device views (u, p) of ghost set gi's target rows."""
+        kind, off, n = self.ghost_slices[gi]
+        g = self.ghost[kind]
+        return g["tu"][off : off + n], g["tp"][off : off + n]
+
+    def set_ghost_targets(self, values):
+        """values aligned with datasets.ghosts: (u (g, n_vel), p (g,)) arrays/tensors."""
+        nv = self.regime.n_vel
+        for gi, (kind, off, n) in self.ghost_slices.items():
+            u, p = values[gi]
+            u_t = u if torch.is_tensor(u) else torch.as_tensor(np.asarray(u, dtype=np.float64))
+            p_t = p if torch.is_tensor(p) else torch.as_tensor(np.asarray(p, dtype=np.float64))
+            if tuple(u_t.shape) != (n, nv) or tuple(p_t.shape) != (n,):
+                raise ValueError("ghost target shape mismatch")
+            tu, tp = self.target_slice(gi)
+            tu.copy_(u_t)
+            tp.copy_(p_t)
+        for kind in self.ghost:
+            self.targets_set[kind] = True
+
+    def mark_targets_set(self):
+        for kind in self.ghost:
+            self.targets_set[kind] = True
+
+    # -- launches -------------------------------------------------------------
+    def loss_coeffs(self):
+        w = self.weights
+        return dict(n_obs=float(self.n_obs), n_colloc=float(self.n_colloc),
+                    n_ghost_total=float(self.n_ghost_total), n_ghost_space=float(self.n_ghost["spatial"]),
+                    n_ghost_time=float(self.n_ghost["temporal"]), w_obs=w.obs, w_pde=w.pde,
+                    w_ghost_u=w.ghost_u, w_ghost_p_space=w.ghost_p_space, w_ghost_p_time=w.ghost_p_time)
+
+    def enqueue(self, kparams, stream=None, part="all"):
+        """Launch the epoch's loss/gradient kernels and reductions (no sync).
+
+        part: "all"; "interior" = obs + PDE heads (independent of the ghost
+        exchange); "rest" = ghost heads + fixed-order reductions."""
+        interior = part in ("all", "interior")
+        rest = part in ("all", "rest")
+        if rest:
+            for kind in self.ghost:
+                if not self.targets_set[kind]:
+                    raise RuntimeError(f"{kind} ghost targets were never set; run an exchange first")
+        plan, npad = self.plan, self.plan.info.np_pad
+        st = X.stream_ptr(stream)
+        kp = X.ptr(kparams)
+        sc = X.ptr(self.scratch)
+        for seg, mode, n, row, ws in self.segments:
+            is_ghost = seg in (SEG_GS, SEG_GT)
+            if (is_ghost and not rest) or (not is_ghost and not interior):
+                continue
+            gp = self.gpart.data_ptr() + 8 * row * npad
+            lp = self.lpart.data_ptr() + 8 * 2 * row
+            if mode == X.MODE_PDE:
+                X.call("fr_pde_fwd_bwd", plan.h, kp, X.ptr(self.col_pts), n,
+                       self.weights.pde / self.n_colloc, gp, lp, sc, st)
+            elif seg == SEG_OBS:
+                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(self.obs_pts), X.ptr(self.obs_vel), None, n,
+                       self.vel_w, self.weights.obs / self.n_obs, 0.0, gp, lp, sc, st)
+            else:
+                g = self.ghost["spatial" if seg == SEG_GS else "temporal"]
+                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(g["pts"]), X.ptr(g["tu"]), X.ptr(g["tp"]), n,
+                       self.vel_w, g["vel_coef"], g["p_coef"], gp, lp, sc, st)
+        if rest:
+            X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0, st)
+            X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
+
+    def parts_from_sums(self, sums):
+        """Unweighted LossParts from the reduced sums (objective.py:183-191)."""
+        s = [float(v) for v in sums]
+        ng = self.n_ghost
+        return LossParts(
+            obs=s[0] / self.n_obs if self.n_obs else 0.0,
+            pde=s[2] / self.n_colloc,
+            ghost_u=(s[4] + s[6]) / self.n_ghost_total if self.n_ghost_total else 0.0,
+            ghost_p_space=s[5] / ng["spatial"] if ng["spatial"] else 0.0,
+            ghost_p_time=s[7] / ng["temporal"] if ng["temporal"] else 0.0,
+        )
+
+
+class LocalObjective:
+    """Drop-in `LocalObjective(config, regime, datasets, weights, batch_size)`.
+
+    `epoch(params, rng, grad_out=None) -> (LossParts, grad, total)` runs on the
+    GPU; `params` is an ExpertParams (or flat f64 vector) and the returned grad
+    is a float64 numpy vector in the reference's flat layout.
+    """
+
+    def __init__(self, config, regime, datasets, weights, batch_size, dtype="float32"):
+        if batch_size < 1:
+            raise ValueError("batch size must be >= 1")
+        self.config = config
+        self.regime = regime
+        self.weights = weights
+        self.batch = int(batch_size)
+        self.plan = get_plan(config, regime.kind, regime.reynolds, dtype)
+        self.dev = DeviceObjective(self.plan, regime, datasets, weights)
+        self.n_obs, self.n_colloc = self.dev.n_obs, self.dev.n_colloc
+        self.n_ghost, self.n_ghost_total = self.dev.n_ghost, self.dev.n_ghost_total
+        self.n_params = config.n_params
+        self._kp = new_kparams(self.plan)
+
+    def set_ghost_targets(self, values):
+        self.dev.set_ghost_targets(values)
+
+    def epoch(self, params, rng=None, grad_out=None):
+        flat = params.flat if hasattr(params, "flat") else np.asarray(params, dtype=np.float64)
+        flat_d = to_device(flat, torch.float64, self.plan.device)
+        if not torch.isfinite(flat_d).all():
+            raise ValueError("non-finite value in parameter")
+        prepare(self.plan, flat_d, self._kp)
+        self.dev.enqueue(self._kp)
+        grad = self.dev.grad.cpu().numpy()
+        parts = self.dev.parts_from_sums(self.dev.sums.cpu().numpy())
+        if grad_out is None:
+            grad_out = np.zeros(self.n_params)
+        grad_out += grad
+        total = compose_loss(parts, self.weights)
+        if not np.isfinite(total):
+            raise FloatingPointError(
+                f"non-finite training loss: obs={parts.obs} pde={parts.pde} ghost_u={parts.ghost_u} "
+                f"ghost_p_space={parts.ghost_p_space} ghost_p_time={parts.ghost_p_time}"
+            )
+        return parts, grad_out, total
