@@ -115,10 +115,13 @@ struct JetCfg {
   static constexpr int SIN = (ACT == ACT_SIN) ? 1 : 0;
   static constexpr int NST0 = 1 + SIN;                       // layer-0 stash / (point,unit)
   static constexpr int NSTH = JET ? (1 + SIN + NG + NL) : NST0;  // hidden-layer stash
-  static constexpr int RS2_BASE = 2 * ROWS;
-  static constexpr int RS2 = sizeof(T) == 4 ? RS2_BASE + ((4 - RS2_BASE % 32) + 32) % 32
-                                            : RS2_BASE + ((2 - RS2_BASE % 16) + 16) % 16;
-  static constexpr int XELEMS = (W / 2) * RS2;
+  // k-quad layout: element (row, k) at (k>>2)*RS4 + row*4 + (k&3).  RS4 is
+  // padded so that consecutive quads start 4 banks apart: the 8 lanes of a
+  // quarter-warp touching 8 consecutive quads then cover all 32 banks.
+  static constexpr int RS4_BASE = 4 * ROWS;
+  static constexpr int RS4 = sizeof(T) == 4 ? RS4_BASE + ((4 - RS4_BASE % 32) + 32) % 32
+                                            : RS4_BASE + ((2 - RS4_BASE % 16) + 16) % 16;
+  static constexpr int XELEMS = (W / 4) * RS4;
   static_assert(W % 8 == 0, "width must be a multiple of 8");
   static_assert(NT % G == 0, "thread count must be divisible by unit groups");
   static_assert(ROWS % 2 == 0, "tile rows must be even");
@@ -149,65 +152,81 @@ struct JetCfg {
   }
 };
 
-// element (row, k) of a k-pair buffer
-template <int RS2>
-__device__ __forceinline__ int kpi(int row, int k) {
-  return (k >> 1) * RS2 + row * 2 + (k & 1);
+// element (row, k) of a k-quad buffer
+template <int RS4>
+__device__ __forceinline__ int kqi(int row, int k) {
+  return (k >> 2) * RS4 + row * 4 + (k & 3);
 }
 
-// acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][8g + j]
-template <typename T, int W, int RPT, int RS2>
+// Units owned by unit-group g: {4g..4g+3} and {W/2+4g..W/2+4g+3}.  A
+// quarter-warp (8 consecutive g) then reads one contiguous 128-byte row
+// segment of a weight matrix per LDS.128 -- conflict-free.
+template <int W>
+__device__ __forceinline__ int unit_of(int g, int j) {
+  return (j < 4) ? 4 * g + j : W / 2 + 4 * g + (j - 4);
+}
+
+// fire-and-forget f64 add into a gradient partial.  Every address of a CTA's
+// partial row has exactly one writer thread per phase, and same-thread
+// operations to one location stay in program order, so the result is the
+// same fixed-order sum on every run.
+__device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
+
+// acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][unit_of(g, j)]
+template <typename T, int W, int RPT, int RS4>
 __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
                                           T (&acc)[RPT][8]) {
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[r][j] = T(0);
-  const T* ap = A + rg * (2 * RPT);
-  const T* bp = B + 8 * g;
-#pragma unroll 4
-  for (int kp = 0; kp < W / 2; ++kp) {
-    T av[2 * RPT];
-    vload(av, ap + kp * RS2);
-    T b0[8], b1[8];
-    vload(b0, bp + (2 * kp) * W);
-    vload(b1, bp + (2 * kp + 1) * W);
+  const T* ap = A + rg * (4 * RPT);
+  const T* bp = B + 4 * g;
+#pragma unroll 2
+  for (int kq = 0; kq < W / 4; ++kq) {
+    T av[4 * RPT];
+    vload(av, ap + kq * RS4);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      T b0[4], b1[4];
+      vload(b0, bp + (4 * kq + kk) * W);
+      vload(b1, bp + (4 * kq + kk) * W + W / 2);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[r][j] = fma(av[4 * r + kk], b0[j], acc[r][j]);
+          acc[r][4 + j] = fma(av[4 * r + kk], b1[j], acc[r][4 + j]);
+        }
+      }
+    }
+  }
+}
+
+// store a thread's [RPT][8] block (rows rg*RPT.., units unit_of(g, .)) into a k-quad buffer
+template <typename T, int W, int RPT, int RS4>
+__device__ __forceinline__ void store_block(T* __restrict__ buf, int rg, int g, const T (&v)[RPT][8]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    T tmp[4 * RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        acc[r][j] = fma(av[2 * r], b0[j], acc[r][j]);
-        acc[r][j] = fma(av[2 * r + 1], b1[j], acc[r][j]);
-      }
+      for (int c = 0; c < 4; ++c) tmp[4 * r + c] = v[r][4 * h + c];
+    vstore(buf + (g + h * (W / 8)) * RS4 + rg * (4 * RPT), tmp);
   }
 }
 
-// store a thread's [RPT][8] block (rows rg*RPT.., units 8g..8g+7) into a k-pair buffer
-template <typename T, int RPT, int RS2>
-__device__ __forceinline__ void store_block(T* __restrict__ buf, int rg, int g, const T (&v)[RPT][8]) {
-#pragma unroll
-  for (int jp = 0; jp < 4; ++jp) {
-    T tmp[2 * RPT];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      tmp[2 * r] = v[r][2 * jp];
-      tmp[2 * r + 1] = v[r][2 * jp + 1];
-    }
-    vstore(buf + (4 * g + jp) * RS2 + rg * (2 * RPT), tmp);
-  }
-}
-
-template <typename T, int RPT, int RS2>
+template <typename T, int W, int RPT, int RS4>
 __device__ __forceinline__ void load_block(T (&v)[RPT][8], const T* __restrict__ buf, int rg, int g) {
 #pragma unroll
-  for (int jp = 0; jp < 4; ++jp) {
-    T tmp[2 * RPT];
-    vload(tmp, buf + (4 * g + jp) * RS2 + rg * (2 * RPT));
+  for (int h = 0; h < 2; ++h) {
+    T tmp[4 * RPT];
+    vload(tmp, buf + (g + h * (W / 8)) * RS4 + rg * (4 * RPT));
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      v[r][2 * jp] = tmp[2 * r];
-      v[r][2 * jp + 1] = tmp[2 * r + 1];
-    }
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[r][4 * h + c] = tmp[4 * r + c];
   }
 }
 
@@ -219,7 +238,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
   using C = JetCfg<T, ACT, MODE, REG, W>;
   constexpr int NT = C::NT, G = C::G, RPT = C::RPT, ROWS = C::ROWS, PPT = C::PPT;
   constexpr int DIN = C::DIN, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
-  constexpr int NG = C::NG, NL = C::NL, LAP0 = C::LAP0, RS2 = C::RS2;
+  constexpr int NG = C::NG, NL = C::NL, LAP0 = C::LAP0, RS4 = C::RS4;
   constexpr int NST0 = C::NST0, NSTH = C::NSTH, PP = C::PP;
   constexpr bool JET = C::JET, BWD = C::BWD;
 
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       T outv[RPT][8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int u = 8 * g + j;
+        const int u = unit_of<W>(g, j);
         const T b0 = Bs[u];
 #pragma unroll
         for (int pr = 0; pr < PP; ++pr) {
@@ -345,7 +364,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
           }
         }
       }
-      store_block<T, RPT, RS2>(Xs, rg, g, outv);
+      store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
     }
     __syncthreads();
 
@@ -354,12 +373,12 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       const T* Bm = (ws & 1) ? slot1 : slot0;
       stage(ws + 1);
       T acc[RPT][8];
-      gemm_rows<T, W, RPT, RS2>(Xs, Bm, rg, g, acc);
+      gemm_rows<T, W, RPT, RS4>(Xs, Bm, rg, g, acc);
       __syncthreads();
       T outv[RPT][8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int u = 8 * g + j;
+        const int u = unit_of<W>(g, j);
         const T bl = Bs[l * W + u];
         if constexpr (JET) {
           const T zv = acc[0][j] + bl;
@@ -397,7 +416,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
           }
         }
       }
-      store_block<T, RPT, RS2>(Xs, rg, g, outv);
+      store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
       cp_async_wait_all();
       __syncthreads();
       ++ws;
@@ -408,15 +427,14 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       T y[NOUT];
 #pragma unroll
       for (int c = 0; c < NOUT; ++c) y[c] = T(0);
-#pragma unroll 8
-      for (int kp2 = 0; kp2 < W / 2; ++kp2) {
-        T xv[2];
-        vload(xv, Xs + kp2 * RS2 + r * 2);
+#pragma unroll 4
+      for (int kq = 0; kq < W / 4; ++kq) {
+        T xv[4];
+        vload(xv, Xs + kq * RS4 + r * 4);
 #pragma unroll
-        for (int c = 0; c < NOUT; ++c) {
-          y[c] = fma(xv[0], WLs[(2 * kp2) * NOUT + c], y[c]);
-          y[c] = fma(xv[1], WLs[(2 * kp2 + 1) * NOUT + c], y[c]);
-        }
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int c = 0; c < NOUT; ++c) y[c] = fma(xv[kk], WLs[(4 * kq + kk) * NOUT + c], y[c]);
       }
       const bool vrow = JET ? (r % S == 0) : true;
 #pragma unroll
@@ -530,19 +548,19 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       for (int i = tid; i < W * NOUT; i += NT) {
         const int k = i / NOUT, c = i % NOUT;
         T s = T(0);
-        for (int r = 0; r < ROWS; ++r) s = fma(Xs[kpi<RS2>(r, k)], Ybs[r * NOUT + c], s);
-        gp[pl.off_w(L) + i] += double(s);
+        for (int r = 0; r < ROWS; ++r) s = fma(Xs[kqi<RS4>(r, k)], Ybs[r * NOUT + c], s);
+        red_add(gp + pl.off_w(L) + i, double(s));
       }
       if (tid < NOUT) {
         T s = T(0);
         for (int pt = 0; pt < PPT; ++pt) s += Ybs[(JET ? pt * S : pt) * NOUT + tid];
-        gp[pl.off_b(L) + tid] += double(s);
+        red_add(gp + pl.off_b(L) + tid, double(s));
       }
       {
         T gv[RPT][8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int u = 8 * g + j;
+          const int u = unit_of<W>(g, j);
 #pragma unroll
           for (int r = 0; r < RPT; ++r) {
             const int row = rg * RPT + r;
@@ -552,7 +570,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
             gv[r][j] = s;
           }
         }
-        store_block<T, RPT, RS2>(Gs, rg, g, gv);
+        store_block<T, W, RPT, RS4>(Gs, rg, g, gv);
       }
       __syncthreads();
 
@@ -561,7 +579,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
         // activation backward (numpy_backend.py:58-89): S-bar -> Z-bar, in place in Gs
         {
           T sb[RPT][8];
-          load_block<T, RPT, RS2>(sb, Gs, rg, g);
+          load_block<T, W, RPT, RS4>(sb, Gs, rg, g);
           T zb[RPT][8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -605,7 +623,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
               }
             }
           }
-          store_block<T, RPT, RS2>(Gs, rg, g, zb);
+          store_block<T, W, RPT, RS4>(Gs, rg, g, zb);
         }
         // rebuild this layer's input H_l = jets of layer l-1 into Xs
         {
@@ -613,7 +631,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
           const int lp = l - 1;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int u = 8 * g + j;
+            const int u = unit_of<W>(g, j);
             if constexpr (JET) {
               const int nst = lp == 0 ? NST0 : NSTH;
               const int q = j * nst;
@@ -649,14 +667,14 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
               for (int r = 0; r < RPT; ++r) hv[r][j] = stash[st_idx(lp, (r * 8 + j) * NST0)];
             }
           }
-          store_block<T, RPT, RS2>(Xs, rg, g, hv);
+          store_block<T, W, RPT, RS4>(Xs, rg, g, hv);
         }
         __syncthreads();
         stage(ws + 1);
 
         // dW_l = H_l^T Zbar_l over all rows of the tile (thread tile 4k x 4u)
         {
-          constexpr int Q = W / 4;
+          constexpr int Q = W / 4;  // k / u quads
           for (int t = tid; t < Q * Q; t += NT) {
             const int kq = t % Q, uq = t / Q;
             T acc[4][4];
@@ -664,48 +682,37 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
             for (int x = 0; x < 4; ++x)
 #pragma unroll
               for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
-            const T* x0p = Xs + kq * RS2;
-            const T* x1p = Xs + (kq + Q) * RS2;
-            const T* z0p = Gs + uq * RS2;
-            const T* z1p = Gs + (uq + Q) * RS2;
+            const T* xp = Xs + kq * RS4;
+            const T* zp = Gs + uq * RS4;
 #pragma unroll 4
-            for (int r = 0; r < ROWS; r += 2) {
-              T x0[4], x1[4], z0[4], z1[4];
-              vload(x0, x0p + 2 * r);
-              vload(x1, x1p + 2 * r);
-              vload(z0, z0p + 2 * r);
-              vload(z1, z1p + 2 * r);
+            for (int r = 0; r < ROWS; ++r) {
+              T hk[4], zu[4];
+              vload(hk, xp + 4 * r);
+              vload(zu, zp + 4 * r);
 #pragma unroll
-              for (int rr = 0; rr < 2; ++rr) {
-                const T hk[4] = {x0[2 * rr], x0[2 * rr + 1], x1[2 * rr], x1[2 * rr + 1]};
-                const T zu[4] = {z0[2 * rr], z0[2 * rr + 1], z1[2 * rr], z1[2 * rr + 1]};
+              for (int x = 0; x < 4; ++x)
 #pragma unroll
-                for (int x = 0; x < 4; ++x)
-#pragma unroll
-                  for (int y = 0; y < 4; ++y) acc[x][y] = fma(hk[x], zu[y], acc[x][y]);
-              }
+                for (int y = 0; y < 4; ++y) acc[x][y] = fma(hk[x], zu[y], acc[x][y]);
             }
-            const int kk[4] = {2 * kq, 2 * kq + 1, 2 * (kq + Q), 2 * (kq + Q) + 1};
-            const int uu[4] = {2 * uq, 2 * uq + 1, 2 * (uq + Q), 2 * (uq + Q) + 1};
-            const int base = pl.off_w(l);
+            double* dst = gp + pl.off_w(l) + (4 * kq) * W + 4 * uq;
 #pragma unroll
             for (int x = 0; x < 4; ++x)
 #pragma unroll
-              for (int y = 0; y < 4; ++y) gp[base + kk[x] * W + uu[y]] += double(acc[x][y]);
+              for (int y = 0; y < 4; ++y) red_add(dst + x * W + y, double(acc[x][y]));
           }
           if (tid < W) {
             T s = T(0);
-            for (int pt = 0; pt < PPT; ++pt) s += Gs[kpi<RS2>(JET ? pt * S : pt, tid)];
-            gp[pl.off_b(l) + tid] += double(s);
+            for (int pt = 0; pt < PPT; ++pt) s += Gs[kqi<RS4>(JET ? pt * S : pt, tid)];
+            red_add(gp + pl.off_b(l) + tid, double(s));
           }
         }
         // dX: S-bar_{l-1} = Zbar_l W_l^T
         {
           const T* Bm = (ws & 1) ? slot1 : slot0;
           T acc[RPT][8];
-          gemm_rows<T, W, RPT, RS2>(Gs, Bm, rg, g, acc);
+          gemm_rows<T, W, RPT, RS4>(Gs, Bm, rg, g, acc);
           __syncthreads();
-          store_block<T, RPT, RS2>(Gs, rg, g, acc);
+          store_block<T, W, RPT, RS4>(Gs, rg, g, acc);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -715,11 +722,11 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       // ---------------- layer 0 backward ----------------
       {
         T sb[RPT][8];
-        load_block<T, RPT, RS2>(sb, Gs, rg, g);
+        load_block<T, W, RPT, RS4>(sb, Gs, rg, g);
         T zb[RPT][8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int u = 8 * g + j;
+          const int u = unit_of<W>(g, j);
           if constexpr (JET) {
             const T s = stash[st_idx(0, j * NST0)];
             const T c = C::SIN ? stash[st_idx(0, j * NST0 + 1)] : T(0);
@@ -757,7 +764,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
             }
           }
         }
-        store_block<T, RPT, RS2>(Gs, rg, g, zb);
+        store_block<T, W, RPT, RS4>(Gs, rg, g, zb);
       }
       __syncthreads();
       // dW0 = X^T Zbar over the stacked input (value rows hold the points, the
@@ -768,13 +775,13 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
         if (j < DIN) {
           for (int pt = 0; pt < PPT; ++pt) {
             const int row = JET ? pt * S : pt;
-            s = fma(Ps[pt * DIN + j], Gs[kpi<RS2>(row, u)], s);
-            if constexpr (JET) s += Gs[kpi<RS2>(row + 1 + j, u)];
+            s = fma(Ps[pt * DIN + j], Gs[kqi<RS4>(row, u)], s);
+            if constexpr (JET) s += Gs[kqi<RS4>(row + 1 + j, u)];
           }
-          gp[pl.off_w(0) + j * W + u] += double(s);
+          red_add(gp + pl.off_w(0) + j * W + u, double(s));
         } else {
-          for (int pt = 0; pt < PPT; ++pt) s += Gs[kpi<RS2>(JET ? pt * S : pt, u)];
-          gp[pl.off_b(0) + u] += double(s);
+          for (int pt = 0; pt < PPT; ++pt) s += Gs[kqi<RS4>(JET ? pt * S : pt, u)];
+          red_add(gp + pl.off_b(0) + u, double(s));
         }
       }
       __syncthreads();
