@@ -122,6 +122,13 @@ struct JetCfg {
   static constexpr int RS4 = sizeof(T) == 4 ? RS4_BASE + ((4 - RS4_BASE % 32) + 32) % 32
                                             : RS4_BASE + ((2 - RS4_BASE % 16) + 16) % 16;
   static constexpr int XELEMS = (W / 4) * RS4;
+  // dW phase: (W/8)^2 thread tiles of 8k x 8u, RSPLIT row ranges combined in
+  // the (then free) activation buffer
+  static constexpr int KT = W / 8;
+  static constexpr int rsplit_fit(int r) {
+    return (r > 1 && (r * KT * KT > NT || (r - 1) * W * W > XELEMS || ROWS % r != 0)) ? rsplit_fit(r / 2) : r;
+  }
+  static constexpr int RSPLIT = rsplit_fit(64);
   static_assert(W % 8 == 0, "width must be a multiple of 8");
   static_assert(NT % G == 0, "thread count must be divisible by unit groups");
   static_assert(ROWS % 2 == 0, "tile rows must be even");
@@ -547,9 +554,13 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
       // ---------------- output layer backward ----------------
       for (int i = tid; i < W * NOUT; i += NT) {
         const int k = i / NOUT, c = i % NOUT;
-        T s = T(0);
-        for (int r = 0; r < ROWS; ++r) s = fma(Xs[kqi<RS4>(r, k)], Ybs[r * NOUT + c], s);
-        red_add(gp + pl.off_w(L) + i, double(s));
+        T s4[4] = {T(0), T(0), T(0), T(0)};  // four independent chains
+        static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
+#pragma unroll 2
+        for (int r = 0; r < ROWS; r += 4)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s4[q] = fma(Xs[kqi<RS4>(r + q, k)], Ybs[(r + q) * NOUT + c], s4[q]);
+        red_add(gp + pl.off_w(L) + i, double((s4[0] + s4[1]) + (s4[2] + s4[3])));
       }
       if (tid < NOUT) {
         T s = T(0);
@@ -672,38 +683,77 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
         __syncthreads();
         stage(ws + 1);
 
-        // dW_l = H_l^T Zbar_l over all rows of the tile (thread tile 4k x 4u)
+        // dW_l = H_l^T Zbar_l over all rows of the tile.  Thread tile 8k x 8u
+        // (k quads {kt, kt+W/8}, u quads {ut, ut+W/8}) over one of RSPLIT row
+        // ranges; a quarter-warp shares kt (broadcast H) and spans 8 ut (one
+        // conflict-free 128-byte Zbar segment).  Row-range partials are combined
+        // through shared memory in a fixed order, then red.add-ed once.
         {
-          constexpr int Q = W / 4;  // k / u quads
-          for (int t = tid; t < Q * Q; t += NT) {
-            const int kq = t % Q, uq = t / Q;
-            T acc[4][4];
+          constexpr int KT = C::KT, RSPLIT = C::RSPLIT, RROWS = ROWS / RSPLIT;
+          const bool active = tid < KT * KT * RSPLIT;
+          const int ut = tid % KT, kt = (tid / KT) % KT, rs = tid / (KT * KT);
+          T acc[8][8];
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
+          for (int x = 0; x < 8; ++x)
 #pragma unroll
-              for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
-            const T* xp = Xs + kq * RS4;
-            const T* zp = Gs + uq * RS4;
-#pragma unroll 4
-            for (int r = 0; r < ROWS; ++r) {
-              T hk[4], zu[4];
-              vload(hk, xp + 4 * r);
-              vload(zu, zp + 4 * r);
+            for (int y = 0; y < 8; ++y) acc[x][y] = T(0);
+          if (active) {
+            const T* x0 = Xs + kt * RS4 + 4 * (rs * RROWS);
+            const T* x1 = Xs + (kt + KT) * RS4 + 4 * (rs * RROWS);
+            const T* z0 = Gs + ut * RS4 + 4 * (rs * RROWS);
+            const T* z1 = Gs + (ut + KT) * RS4 + 4 * (rs * RROWS);
+#pragma unroll 2
+            for (int r = 0; r < RROWS; ++r) {
+              T h[8], z[8];
+              vload(*reinterpret_cast<T(*)[4]>(h), x0 + 4 * r);
+              vload(*reinterpret_cast<T(*)[4]>(h + 4), x1 + 4 * r);
+              vload(*reinterpret_cast<T(*)[4]>(z), z0 + 4 * r);
+              vload(*reinterpret_cast<T(*)[4]>(z + 4), z1 + 4 * r);
 #pragma unroll
-              for (int x = 0; x < 4; ++x)
+              for (int x = 0; x < 8; ++x)
 #pragma unroll
-                for (int y = 0; y < 4; ++y) acc[x][y] = fma(hk[x], zu[y], acc[x][y]);
+                for (int y = 0; y < 8; ++y) acc[x][y] = fma(h[x], z[y], acc[x][y]);
             }
-            double* dst = gp + pl.off_w(l) + (4 * kq) * W + 4 * uq;
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-              for (int y = 0; y < 4; ++y) red_add(dst + x * W + y, double(acc[x][y]));
           }
           if (tid < W) {
-            T s = T(0);
-            for (int pt = 0; pt < PPT; ++pt) s += Gs[kqi<RS4>(JET ? pt * S : pt, tid)];
-            red_add(gp + pl.off_b(l) + tid, double(s));
+            T sb = T(0);
+            for (int pt = 0; pt < PPT; ++pt) sb += Gs[kqi<RS4>(JET ? pt * S : pt, tid)];
+            red_add(gp + pl.off_b(l) + tid, double(sb));
+          }
+          __syncthreads();  // every read of Xs (H_l) is done: reuse it as scratch
+          auto kidx = [&](int x) { return x < 4 ? 4 * kt + x : 4 * (kt + KT) + (x - 4); };
+          if (active && rs > 0) {
+            T* dst = Xs + (rs - 1) * W * W;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              const int k = kidx(x);
+              vstore(dst + k * W + 4 * ut, *reinterpret_cast<const T(*)[4]>(&acc[x][0]));
+              vstore(dst + k * W + 4 * (ut + KT), *reinterpret_cast<const T(*)[4]>(&acc[x][4]));
+            }
+          }
+          __syncthreads();
+          if (active && rs == 0) {
+            double* dst = gp + pl.off_w(l);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              const int k = kidx(x);
+              for (int q = 1; q < RSPLIT; ++q) {
+                const T* src = Xs + (q - 1) * W * W + k * W;
+                T a4[4], b4[4];
+                vload(a4, src + 4 * ut);
+                vload(b4, src + 4 * (ut + KT));
+#pragma unroll
+                for (int y = 0; y < 4; ++y) {
+                  acc[x][y] += a4[y];
+                  acc[x][4 + y] += b4[y];
+                }
+              }
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                red_add(dst + k * W + 4 * ut + y, double(acc[x][y]));
+                red_add(dst + k * W + 4 * (ut + KT) + y, double(acc[x][4 + y]));
+              }
+            }
           }
         }
         // dX: S-bar_{l-1} = Zbar_l W_l^T
