@@ -106,7 +106,9 @@ struct JetCfg {
   static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0, RPT = St::RPT;
   static constexpr bool JET = St::JET;
   static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE);
-  static constexpr int NT = sizeof(T) == 4 ? 256 : 128;
+  // 12 warps per SM where the FP32 tile buffers still fit (W = 64, <= 6 streams);
+  // otherwise 8 (FP32) or 4 (FP64 parity build)
+  static constexpr int NT = sizeof(T) == 4 ? ((W == 64 && St::RPT <= 6) ? 384 : 256) : 128;
   static constexpr int G = W / 8;          // unit groups of 8 per row group
   static constexpr int NRG = NT / G;       // row groups
   static constexpr int ROWS = NRG * RPT;   // rows per tile
@@ -125,10 +127,12 @@ struct JetCfg {
   // dW phase: (W/8)^2 thread tiles of 8k x 8u, RSPLIT row ranges combined in
   // the (then free) activation buffer
   static constexpr int KT = W / 8;
+  // largest split with one thread per (tile, range), rows divisible, and the
+  // R-1 partials of the flat combine fitting in the activation buffer
   static constexpr int rsplit_fit(int r) {
-    return (r > 1 && (r * KT * KT > NT || (r - 1) * W * W > XELEMS || ROWS % r != 0)) ? rsplit_fit(r / 2) : r;
+    return (r > 1 && (r * KT * KT > NT || (r - 1) * W * W > XELEMS || ROWS % r != 0)) ? rsplit_fit(r - 1) : r;
   }
-  static constexpr int RSPLIT = rsplit_fit(64);
+  static constexpr int RSPLIT = rsplit_fit(NT / (KT * KT) > 0 ? NT / (KT * KT) : 1);
   static_assert(W % 8 == 0, "width must be a multiple of 8");
   static_assert(NT % G == 0, "thread count must be divisible by unit groups");
   static_assert(ROWS % 2 == 0, "tile rows must be even");
@@ -721,14 +725,14 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
             red_add(gp + pl.off_b(l) + tid, double(sb));
           }
           __syncthreads();  // every read of Xs (H_l) is done: reuse it as scratch
+          // combine the RSPLIT row-range partials in a fixed order (rs = 1, 2, ...)
           auto kidx = [&](int x) { return x < 4 ? 4 * kt + x : 4 * (kt + KT) + (x - 4); };
           if (active && rs > 0) {
             T* dst = Xs + (rs - 1) * W * W;
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
-              const int k = kidx(x);
-              vstore(dst + k * W + 4 * ut, *reinterpret_cast<const T(*)[4]>(&acc[x][0]));
-              vstore(dst + k * W + 4 * (ut + KT), *reinterpret_cast<const T(*)[4]>(&acc[x][4]));
+              vstore(dst + kidx(x) * W + 4 * ut, *reinterpret_cast<const T(*)[4]>(&acc[x][0]));
+              vstore(dst + kidx(x) * W + 4 * (ut + KT), *reinterpret_cast<const T(*)[4]>(&acc[x][4]));
             }
           }
           __syncthreads();
