@@ -92,9 +92,12 @@ int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long
 int fr_jet_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,
                fr_stream_t stream);
 
-/* grad[i] (+)= sum_rows gpart[row][pad(i)], fixed row order */
+/* grad[i] (+)= sum_rows gpart[row][pad(i)], fixed row order; when norm_parts is
+ * non-NULL also writes per-block partial sums of grad^2 (fr_reduce_grad_parts()
+ * entries) for fr_adam_step */
 int fr_reduce_grad(const fr_plan* plan, const double* gpart, int rows, double* grad, int accumulate,
-                   fr_stream_t stream);
+                   double* norm_parts, fr_stream_t stream);
+int fr_reduce_grad_parts(const fr_plan* plan);
 /* sums[2*s + c] = sum over rows of segment s of lpart[2*row + c], fixed order */
 int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int n_seg, double* sums,
                    fr_stream_t stream);
@@ -113,17 +116,21 @@ typedef struct {
   const double* sched;
   long long row_base;
   double beta1, beta2, eps, clip_norm; /* clip_norm <= 0: no clipping */
-  /* loss bookkeeping (NULL -> no history / finiteness check): fr_reduce_loss
-   * output over the segments {obs, pde, ghost-spatial, ghost-temporal}, i.e.
-   * sums[8] = {obs sq_u, -, pde sq, -, gs sq_u, gs sq_p, gt sq_u, gt sq_p} */
-  const double* loss_sums;
+  /* squared-norm partials written by fr_reduce_grad (NULL: reduce grad here) */
+  const double* norm_parts;
+  int n_norm_parts;
+  /* loss bookkeeping (lpart == NULL -> no history / finiteness check): per-CTA
+   * loss partial rows of the datasets {obs, pde, ghost-spatial, ghost-temporal},
+   * seg_rows[s] rows each, contiguous in that order */
+  const double* lpart;
+  int seg_rows[4];
   double n_obs, n_colloc, n_ghost_total, n_ghost_space, n_ghost_time;
   double w_obs, w_pde, w_ghost_u, w_ghost_p_space, w_ghost_p_time;
   double* history;          /* rows of 7: epoch, 5 unweighted parts, lr */
   int* flags;               /* FR_FLAG_* bits, sticky */
-  double* grad_norm;        /* optional: pre-clip norm per step (indexed by step) */
-  /* optional: refresh prepared kernel params after the update */
-  void* kparams;
+  double* grad_norm;        /* optional: pre-clip norm per step (row index) */
+  void* kparams;            /* optional: refresh prepared kernel params */
+  int* sync_counter;        /* device int, zero-initialised, self-resetting */
 } fr_adam_args;
 
 /* plan may be NULL when kparams is NULL (plain flat-vector Adam) */

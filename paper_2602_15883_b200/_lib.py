@@ -51,13 +51,14 @@ class AdamArgs(C.Structure):
         ("params", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p),
         ("step", C.c_void_p), ("sched", C.c_void_p), ("row_base", C.c_longlong),
         ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("clip_norm", C.c_double),
-        ("loss_sums", C.c_void_p),
+        ("norm_parts", C.c_void_p), ("n_norm_parts", C.c_int),
+        ("lpart", C.c_void_p), ("seg_rows", C.c_int * 4),
         ("n_obs", C.c_double), ("n_colloc", C.c_double), ("n_ghost_total", C.c_double),
         ("n_ghost_space", C.c_double), ("n_ghost_time", C.c_double),
         ("w_obs", C.c_double), ("w_pde", C.c_double), ("w_ghost_u", C.c_double),
         ("w_ghost_p_space", C.c_double), ("w_ghost_p_time", C.c_double),
         ("history", C.c_void_p), ("flags", C.c_void_p), ("grad_norm", C.c_void_p),
-        ("kparams", C.c_void_p),
+        ("kparams", C.c_void_p), ("sync_counter", C.c_void_p),
     ]
 
 
@@ -73,7 +74,8 @@ _SIGS = {
     "fr_mse_fwd_bwd": [_P, _P, _P, _P, _P, C.c_longlong, _P, C.c_double, C.c_double, _P, _P, _P, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
-    "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P],
+    "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
+    "fr_reduce_grad_parts": [_P],
     "fr_reduce_loss": [_P, C.POINTER(C.c_int), C.c_int, _P, _P],
     "fr_adam_step": [_P, C.POINTER(AdamArgs), _P],
     "fr_pack_ghost": [_P, _P, _P, C.c_longlong, _P, _P, _P],

@@ -46,6 +46,7 @@ struct fr_plan {
   fr_plan_info info;
   ParamLayout pl;
   int* d_map = nullptr;      // real flat index -> padded index      [n_params]
+  int* d_mapT = nullptr;     // real flat index -> W^T copy index or -1 [n_params]
   int* d_inv = nullptr;      // kernel-param element -> real index or -1 [kp_elems]
 };
 
@@ -95,7 +96,7 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   I.np_pad = p->pl.np_pad();
   I.kp_elems = p->pl.total();
   // real flat layout W0,b0,W1,b1,... (network.py:112-115)
-  std::vector<int> map;
+  std::vector<int> map, mapT;
   std::vector<int> inv(I.kp_elems, -1);
   for (int l = 0; l <= L; ++l) {
     const int fi = (l == 0) ? din : width;
@@ -105,13 +106,19 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
       for (int o = 0; o < fo; ++o) {
         const int pidx = p->pl.off_w(l) + i * fo_pad + o;
         inv[pidx] = int(map.size());
-        if (l >= 1 && l < L) inv[p->pl.off_wt(l) + o * wpad + i] = int(map.size());
+        int tidx = -1;
+        if (l >= 1 && l < L) {
+          tidx = p->pl.off_wt(l) + o * wpad + i;
+          inv[tidx] = int(map.size());
+        }
         map.push_back(pidx);
+        mapT.push_back(tidx);
       }
     for (int o = 0; o < fo; ++o) {
       const int pidx = p->pl.off_b(l) + o;
       inv[pidx] = int(map.size());
       map.push_back(pidx);
+      mapT.push_back(-1);
     }
   }
   I.n_params = int(map.size());
@@ -120,11 +127,14 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&I.num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_map, sizeof(int) * map.size());
   if (e == cudaSuccess) e = cudaMalloc(&p->d_inv, sizeof(int) * inv.size());
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_mapT, sizeof(int) * mapT.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_mapT, mapT.data(), sizeof(int) * mapT.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_map, map.data(), sizeof(int) * map.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_inv, inv.data(), sizeof(int) * inv.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(p->d_map);
     cudaFree(p->d_inv);
+    cudaFree(p->d_mapT);
     delete p;
     return cuda_fail(e, "fr_plan_create");
   }
@@ -136,6 +146,7 @@ extern "C" int fr_plan_destroy(fr_plan* p) {
   if (!p) return 0;
   cudaFree(p->d_map);
   cudaFree(p->d_inv);
+  cudaFree(p->d_mapT);
   delete p;
   return 0;
 }
@@ -261,23 +272,52 @@ extern "C" int fr_jet_fwd(const fr_plan* p, const void* kparams, const void* pts
 }
 
 // ---------------------------------------------------------------------------
-__global__ void reduce_grad_kernel(const double* __restrict__ gpart, int rows, int np_pad, const int* __restrict__ map,
-                                   int n, double* grad, int accumulate) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int col = map[i];
+// 32 parameters x 8 row groups per block: coalesced 256-byte row reads, the 8
+// partial sums combined in a fixed order, then a fixed-order block sum of g^2
+// for the optimiser's global norm.
+constexpr int RG_P = 32, RG_R = 8;
+__global__ void __launch_bounds__(RG_P * RG_R) reduce_grad_kernel(const double* __restrict__ gpart, int rows, int np_pad,
+                                                                  const int* __restrict__ map, int n, double* grad,
+                                                                  int accumulate, double* norm_parts) {
+  __shared__ double part[RG_R][RG_P];
+  const int tx = threadIdx.x % RG_P, ty = threadIdx.x / RG_P;
+  const int i = blockIdx.x * RG_P + tx;
   double s = 0.0;
-  for (int r = 0; r < rows; ++r) s += gpart[size_t(r) * np_pad + col];
-  grad[i] = accumulate ? grad[i] + s : s;
+  if (i < n) {
+    const double* col = gpart + map[i];
+    int r = ty;
+#pragma unroll 4
+    for (; r < rows; r += RG_R) s += col[size_t(r) * np_pad];
+  }
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < RG_R; ++q) t += part[q][tx];
+    double g = 0.0;
+    if (i < n) {
+      g = accumulate ? grad[i] + t : t;
+      grad[i] = g;
+    }
+    if (norm_parts) {
+      double sq = g * g;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+      if (tx == 0) norm_parts[blockIdx.x] = sq;
+    }
+  }
 }
 
+extern "C" int fr_reduce_grad_parts(const fr_plan* p) { return p ? (p->info.n_params + RG_P - 1) / RG_P : 0; }
+
 extern "C" int fr_reduce_grad(const fr_plan* p, const double* gpart, int rows, double* grad, int accumulate,
-                              fr_stream_t stream) {
+                              double* norm_parts, fr_stream_t stream) {
   if (!p || !grad || (rows > 0 && !gpart)) return fail("fr_reduce_grad: NULL argument");
   const int n = p->info.n_params;
-  if (rows <= 0 && accumulate) return 0;
-  reduce_grad_kernel<<<(n + 127) / 128, 128, 0, stream>>>(gpart, rows > 0 ? rows : 0, p->info.np_pad, p->d_map, n,
-                                                          grad, accumulate);
+  if (rows <= 0 && accumulate && !norm_parts) return 0;
+  reduce_grad_kernel<<<(n + RG_P - 1) / RG_P, RG_P * RG_R, 0, stream>>>(gpart, rows > 0 ? rows : 0, p->info.np_pad,
+                                                                        p->d_map, n, grad, accumulate, norm_parts);
   FR_CUDA(cudaGetLastError(), "fr_reduce_grad");
   return 0;
 }
@@ -318,105 +358,147 @@ extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int
 
 // ---------------------------------------------------------------------------
 // Adam (optim.py:20-49) with the epoch bookkeeping of objective.py:183-198 and
-// worker.py:231-244.  One CTA; every reduction in a fixed order.  f64 products
-// and sums use explicit round-to-nearest intrinsics so no FMA contraction
-// changes the reference's rounding sequence.
+// worker.py:231-244.  Multi-CTA: every block redundantly forms the global norm
+// and the loss parts from the partials in the same fixed order, updates its
+// slice of parameters and refreshes the kernel copy; the last block to finish
+// advances the step counter.  f64 arithmetic uses explicit round-to-nearest
+// intrinsics so no FMA contraction changes the reference's rounding sequence.
 // ---------------------------------------------------------------------------
+constexpr int ADAM_NT = 256;
+
+__device__ double block_sum_fixed(double v, double* red) {
+  // fixed-shape tree: identical order in every block and on every run
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = ADAM_NT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(1024) adam_kernel(fr_adam_args a, int n, const int* __restrict__ inv, int kp_elems) {
-  __shared__ double red[1024];
-  __shared__ int skip;
+__global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, const int* __restrict__ map,
+                                                       const int* __restrict__ mapT) {
+  __shared__ double red[ADAM_NT];
   const int tid = threadIdx.x;
   const long long step0 = *a.step;  // steps taken so far
   const long long row = step0 - a.row_base;
-  if (tid == 0) {
-    skip = 0;
-    if (a.loss_sums) {
-      const double* s = a.loss_sums;
-      const double obs = a.n_obs > 0 ? s[0] / a.n_obs : 0.0;
-      const double pde = s[2] / a.n_colloc;
-      const double gu = a.n_ghost_total > 0 ? (s[4] + s[6]) / a.n_ghost_total : 0.0;
-      const double gps = a.n_ghost_space > 0 ? s[5] / a.n_ghost_space : 0.0;
-      const double gpt = a.n_ghost_time > 0 ? s[7] / a.n_ghost_time : 0.0;
-      // compose_loss (physics.py:214-224), evaluated left to right
-      double total = __dmul_rn(a.w_obs, obs);
-      total = __dadd_rn(total, __dmul_rn(a.w_pde, pde));
-      total = __dadd_rn(total, __dmul_rn(a.w_ghost_u, gu));
-      total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_space, gps));
-      total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_time, gpt));
+
+  // ---- global gradient norm (optim.py:20-28) ----
+  double acc = 0.0;
+  if (a.norm_parts) {
+    for (int i = tid; i < a.n_norm_parts; i += ADAM_NT) acc = __dadd_rn(acc, a.norm_parts[i]);
+  } else {
+    for (int i = tid; i < n; i += ADAM_NT) acc = __dadd_rn(acc, __dmul_rn(a.grad[i], a.grad[i]));
+  }
+  const double norm = sqrt(block_sum_fixed(acc, red));
+
+  // ---- loss parts, history row, finiteness (objective.py:183-198) ----
+  bool skip = false;
+  if (a.lpart) {
+    double sums[8];
+    int r0 = 0;
+    for (int sgi = 0; sgi < 4; ++sgi) {
+      double x = 0.0, y = 0.0;
+      for (int r = r0 + tid; r < r0 + a.seg_rows[sgi]; r += ADAM_NT) {
+        x += a.lpart[2 * r];
+        y += a.lpart[2 * r + 1];
+      }
+      sums[2 * sgi] = block_sum_fixed(x, red);
+      sums[2 * sgi + 1] = block_sum_fixed(y, red);
+      r0 += a.seg_rows[sgi];
+    }
+    const double obs = a.n_obs > 0 ? sums[0] / a.n_obs : 0.0;
+    const double pde = sums[2] / a.n_colloc;
+    const double gu = a.n_ghost_total > 0 ? (sums[4] + sums[6]) / a.n_ghost_total : 0.0;
+    const double gps = a.n_ghost_space > 0 ? sums[5] / a.n_ghost_space : 0.0;
+    const double gpt = a.n_ghost_time > 0 ? sums[7] / a.n_ghost_time : 0.0;
+    // compose_loss (physics.py:214-224), left to right
+    double total = __dmul_rn(a.w_obs, obs);
+    total = __dadd_rn(total, __dmul_rn(a.w_pde, pde));
+    total = __dadd_rn(total, __dmul_rn(a.w_ghost_u, gu));
+    total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_space, gps));
+    total = __dadd_rn(total, __dmul_rn(a.w_ghost_p_time, gpt));
+    skip = !isfinite(total);
+    if (blockIdx.x == 0 && tid == 0) {
       if (a.history) {
         double* h = a.history + 7 * row;
         h[0] = double(step0);
         h[1] = obs; h[2] = pde; h[3] = gu; h[4] = gps; h[5] = gpt;
         h[6] = a.sched[3 * row];
       }
-      if (!isfinite(total)) {
-        atomicOr(a.flags, FR_FLAG_NONFINITE_LOSS);
-        skip = 1;
-      }
+      if (skip) atomicOr(a.flags, FR_FLAG_NONFINITE_LOSS);
     }
   }
-  double acc = 0.0;
-  for (int i = tid; i < n; i += blockDim.x) acc = __dadd_rn(acc, __dmul_rn(a.grad[i], a.grad[i]));
-  red[tid] = acc;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (tid < w) red[tid] = __dadd_rn(red[tid], red[tid + w]);
-    __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    if (a.grad_norm) a.grad_norm[row] = norm;
+    if (!isfinite(norm)) atomicOr(a.flags, FR_FLAG_NONFINITE_GRAD);
   }
-  const double norm = sqrt(red[0]);
-  if (tid == 0 && a.grad_norm) a.grad_norm[row] = norm;
-  if (!isfinite(norm)) {
-    if (tid == 0) atomicOr(a.flags, FR_FLAG_NONFINITE_GRAD);
-    return;
-  }
-  if (skip) return;
-  const double scale = (a.clip_norm > 0.0 && norm > a.clip_norm) ? a.clip_norm / norm : 1.0;
-  const double lr = a.sched[3 * row];
-  const double bc1 = a.sched[3 * row + 1];
-  const double bc2 = a.sched[3 * row + 2];
-  const double omb1 = 1.0 - a.beta1, omb2 = 1.0 - a.beta2;
-  for (int i = tid; i < n; i += blockDim.x) {
+  skip = skip || !isfinite(norm);
+
+  // ---- update (optim.py:31-49) ----
+  const int i = blockIdx.x * ADAM_NT + tid;
+  if (!skip && i < n) {
+    const double scale = (a.clip_norm > 0.0 && norm > a.clip_norm) ? a.clip_norm / norm : 1.0;
+    const double lr = a.sched[3 * row];
+    const double bc1 = a.sched[3 * row + 1];
+    const double bc2 = a.sched[3 * row + 2];
+    const double omb1 = 1.0 - a.beta1, omb2 = 1.0 - a.beta2;
     double g = a.grad[i];
     if (scale != 1.0) {
       g = __dmul_rn(g, scale);
       a.grad[i] = g;
     }
-    double m = __dadd_rn(__dmul_rn(a.m[i], a.beta1), __dmul_rn(omb1, g));
-    double v = __dadd_rn(__dmul_rn(a.v[i], a.beta2), __dmul_rn(__dmul_rn(omb2, g), g));
+    const double m = __dadd_rn(__dmul_rn(a.m[i], a.beta1), __dmul_rn(omb1, g));
+    const double v = __dadd_rn(__dmul_rn(a.v[i], a.beta2), __dmul_rn(__dmul_rn(omb2, g), g));
     a.m[i] = m;
     a.v[i] = v;
     const double mh = __ddiv_rn(m, bc1);
     const double vh = __ddiv_rn(v, bc2);
     const double upd = __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), a.eps));
-    a.params[i] = __dsub_rn(a.params[i], upd);
+    const double p = __dsub_rn(a.params[i], upd);
+    a.params[i] = p;
+    if (a.kparams) {
+      T* kp = static_cast<T*>(a.kparams);
+      kp[map[i]] = T(p);
+      if (mapT[i] >= 0) kp[mapT[i]] = T(p);
+    }
   }
-  __syncthreads();
-  if (tid == 0) *a.step = step0 + 1;
-  if (a.kparams) {
-    T* kp = static_cast<T*>(a.kparams);
-    for (int i = tid; i < kp_elems; i += blockDim.x) {
-      const int r = inv[i];
-      if (r >= 0) kp[i] = T(a.params[r]);
+  // ---- the last block advances the step counter ----
+  if (!skip) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const int done = atomicAdd(a.sync_counter, 1);
+      if (done == int(gridDim.x) - 1) {
+        *a.step = step0 + 1;
+        *a.sync_counter = 0;
+        __threadfence();
+      }
     }
   }
 }
 
 extern "C" int fr_adam_step(const fr_plan* p, const fr_adam_args* args, fr_stream_t stream) {
   if (!args || !args->params || !args->grad || !args->m || !args->v || !args->step || !args->sched ||
-      !args->flags)
+      !args->flags || !args->sync_counter)
     return fail("fr_adam_step: NULL argument");
   if (args->n < 1 || args->n > (1LL << 30)) return fail("fr_adam_step: bad parameter count %lld", args->n);
   if (args->kparams && !p) return fail("fr_adam_step: refreshing kernel params needs the plan");
   if (p && args->n != p->info.n_params)
     return fail("fr_adam_step: n=%lld does not match the plan's %d parameters", args->n, p->info.n_params);
-  if (args->loss_sums && !(args->n_colloc > 0)) return fail("fr_adam_step: n_colloc must be positive");
-  const int* inv = p ? p->d_inv : nullptr;
-  const int kpe = p ? p->info.kp_elems : 0;
+  if (args->lpart && !(args->n_colloc > 0)) return fail("fr_adam_step: n_colloc must be positive");
+  const int n = int(args->n);
+  const int blocks = (n + ADAM_NT - 1) / ADAM_NT;
+  const int* map = p ? p->d_map : nullptr;
+  const int* mapT = p ? p->d_mapT : nullptr;
   if (!p || p->info.dtype == FR_F32)
-    adam_kernel<float><<<1, 1024, 0, stream>>>(*args, int(args->n), inv, kpe);
+    adam_kernel<float><<<blocks, ADAM_NT, 0, stream>>>(*args, n, map, mapT);
   else
-    adam_kernel<double><<<1, 1024, 0, stream>>>(*args, int(args->n), inv, kpe);
+    adam_kernel<double><<<blocks, ADAM_NT, 0, stream>>>(*args, n, map, mapT);
   FR_CUDA(cudaGetLastError(), "fr_adam_step");
   return 0;
 }

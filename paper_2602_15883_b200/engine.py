@@ -140,7 +140,7 @@ def _train_call(plan, mode, n, launch):
     scratch = torch.empty(max(ws.scratch_bytes, 16), dtype=torch.uint8, device=dev)
     launch(gpart, lpart, scratch)
     grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
-    X.call("fr_reduce_grad", plan.h, X.ptr(gpart), ws.grid, X.ptr(grad), 0, X.stream_ptr())
+    X.call("fr_reduce_grad", plan.h, X.ptr(gpart), ws.grid, X.ptr(grad), 0, None, X.stream_ptr())
     sums = torch.zeros(2, dtype=torch.float64, device=dev)
     rows = (C.c_int * 1)(ws.grid)
     X.call("fr_reduce_loss", X.ptr(lpart), rows, 1, X.ptr(sums), X.stream_ptr())

@@ -98,6 +98,7 @@ class DeviceObjective:
         self.lpart = torch.empty(max(rows, 1) * 2, dtype=torch.float64, device=dev)
         self.scratch = torch.empty(max(scratch, 16), dtype=torch.uint8, device=dev)
         self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
+        self.norm_parts = torch.zeros(X.lib().fr_reduce_grad_parts(plan.h), dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
 
     # -- ghost targets --------------------------------------------------------
@@ -129,16 +130,18 @@ class DeviceObjective:
     # -- launches -------------------------------------------------------------
     def loss_coeffs(self):
         w = self.weights
-        return dict(n_obs=float(self.n_obs), n_colloc=float(self.n_colloc),
+        return dict(lpart=self.lpart, seg_rows=list(self.seg_rows), n_obs=float(self.n_obs), n_colloc=float(self.n_colloc),
                     n_ghost_total=float(self.n_ghost_total), n_ghost_space=float(self.n_ghost["spatial"]),
                     n_ghost_time=float(self.n_ghost["temporal"]), w_obs=w.obs, w_pde=w.pde,
                     w_ghost_u=w.ghost_u, w_ghost_p_space=w.ghost_p_space, w_ghost_p_time=w.ghost_p_time)
 
-    def enqueue(self, kparams, stream=None, part="all"):
+    def enqueue(self, kparams, stream=None, part="all", with_sums=True):
         """Launch the epoch's loss/gradient kernels and reductions (no sync).
 
         part: "all"; "interior" = obs + PDE heads (independent of the ghost
-        exchange); "rest" = ghost heads + fixed-order reductions."""
+        exchange); "rest" = ghost heads + fixed-order reductions.  with_sums
+        also reduces the loss partials into `sums` (the training loop leaves
+        that to the optimiser kernel, which reads the partials directly)."""
         interior = part in ("all", "interior")
         rest = part in ("all", "rest")
         if rest:
@@ -166,8 +169,10 @@ class DeviceObjective:
                 X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(g["pts"]), X.ptr(g["tu"]), X.ptr(g["tp"]), n,
                        self.vel_w, g["vel_coef"], g["p_coef"], gp, lp, sc, st)
         if rest:
-            X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0, st)
-            X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
+            X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
+                   X.ptr(self.norm_parts), st)
+            if with_sums:
+                X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
 
     def parts_from_sums(self, sums):
         """Unweighted LossParts from the reduced sums (objective.py:183-191)."""
