@@ -222,7 +222,7 @@ def run_ours(args):
         t_e2e = float(tt.item())
 
     # ---- dominant kernel: the fused PDE jet-MLP fwd+bwd, timed alone ----
-    pde = _time_pde_kernel(torch, X, worker)
+    pde = _time_epoch_kernel(torch, X, worker)
     peak = measure_fp32_peak(torch, X) if rank == 0 else None
     if dist is not None:
         dist.barrier()
@@ -230,7 +230,8 @@ def run_ours(args):
     if rank == 0:
         n_loc = obj.n_colloc
         fpp = flops_per_point()
-        achieved = fpp * n_loc / pde["ms"] * 1e-9  # TFLOP/s
+        flops_launch = fpp * n_loc + flops_per_value_point() * pde["n_mse"]
+        achieved = flops_launch / pde["ms"] * 1e-9  # TFLOP/s
         clk = clocks.summary()
         line = {
             "metric": METRIC,
@@ -260,11 +261,12 @@ def run_ours(args):
             "launches_per_step": lp,
             "roofline": {
                 "bound": "compute", "pipe": "fp32-simt (FFMA)",
-                "kernel": "jetmlp_kernel<float,tanh,PDE,unsteady2d,64> (fr_pde_fwd_bwd)",
+                "kernel": "jetmlp_epoch_kernel<float,tanh,unsteady2d,64> (fr_epoch_fwd_bwd: PDE + obs/ghost heads)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
                 "peak_source": "measured FP32 FFMA probe (fr_bench_ffma) on this GPU",
-                "flops_per_point": fpp, "points_per_launch": n_loc,
+                "flops_per_point": fpp, "points_per_launch": n_loc, "value_points_per_launch": pde["n_mse"],
+                "flops_per_launch": flops_launch,
                 "kernel_ms": pde["ms"], "kernel_share_of_step": pde["ms"] / (t_rank / args.steps * 1e3),
                 "traffic": None,
             },
@@ -291,16 +293,14 @@ def _launches_per_epoch(trainer, X):
     return n
 
 
-def _time_pde_kernel(torch, X, worker, reps=10):
+def _time_epoch_kernel(torch, X, worker, reps=10):
+    """CUDA-event time of the fused epoch kernel alone (PDE + obs/ghost heads)."""
     obj = worker.objective
-    seg = [s for s in obj.segments if s[1] == X.MODE_PDE][0]
-    _, _, n, row, _ = seg
-    gp = obj.gpart.data_ptr() + 8 * row * worker.plan.info.np_pad
-    lp = obj.lpart.data_ptr() + 16 * row
 
     def launch():
-        X.call("fr_pde_fwd_bwd", worker.plan.h, X.ptr(worker.kp), X.ptr(obj.col_pts), n,
-               obj.weights.pde / obj.n_colloc, gp, lp, X.ptr(obj.scratch), X.stream_ptr())
+        X.call("fr_epoch_fwd_bwd", worker.plan.h, X.ptr(worker.kp), X.ptr(obj.col_pts), obj.n_colloc,
+               obj.weights.pde / obj.n_colloc, obj.sets, len(obj.set_order), obj.vel_w,
+               X.ptr(obj.gpart), obj.lpart_blocks, X.ptr(obj.scratch), X.stream_ptr())
 
     launch()
     torch.cuda.synchronize()
@@ -312,7 +312,13 @@ def _time_pde_kernel(torch, X, worker, reps=10):
         b.record()
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
-    return {"ms": float(np.median(ms)), "n": n}
+    n_mse = sum(obj.sets[i].n for i in range(len(obj.set_order)))
+    return {"ms": float(np.median(ms)), "n": obj.n_colloc, "n_mse": n_mse}
+
+
+def flops_per_value_point(L=4, W=64, d_in=3, n_out=3):
+    """Value-stream MSE head fwd+bwd per point (obs / ghost sets)."""
+    return 6 * (L - 1) * W * W + 6 * d_in * W + 6 * W * n_out + 10 * L * W
 
 
 # ---------------------------------------------------------------------------

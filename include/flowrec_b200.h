@@ -13,6 +13,7 @@
  *   fr_prepare_params     tape.py:314-326 (Tape.bind_params: params bound by reference)
  *   fr_pde_fwd_bwd        builders.py:85-100 build_pde_tape + tape.py:329-371 fwd/bwd
  *   fr_mse_fwd_bwd        builders.py:103-141 build_mse_tape + tape.py:329-371
+ *   fr_epoch_fwd_bwd      runtime/objective.py:164-182 (all of one rank's loss heads)
  *   fr_value_fwd          builders.py:67-73 build_value_tape; network.py:142-156 predict
  *   fr_jet_fwd            builders.py:76-82,192-203 build_jet_tape/forward_jet;
  *                         network.py:162-177 predict_jet
@@ -84,6 +85,27 @@ int fr_pde_fwd_bwd(const fr_plan* plan, const void* kparams, const void* pts, lo
 int fr_mse_fwd_bwd(const fr_plan* plan, const void* kparams, const void* pts, const void* target_u,
                    const void* target_p, long long n, const double* vel_w, double vel_coef,
                    double p_coef, double* gpart, double* lpart, void* scratch, fr_stream_t stream);
+
+/* One launch for a whole epoch's loss heads: the PDE residual over the
+ * collocation points plus up to three MSE sets (obs, ghost-spatial,
+ * ghost-temporal; target_p NULL omits a set's pressure term).  Every CTA adds
+ * all its contributions into one f64 gradient-partial row (gpart: grid rows of
+ * np_pad); loss partials go to per-set blocks of `grid` rows x 2 in lpart:
+ * lpart_blocks[0] <- the PDE, lpart_blocks[1 + s] <- set s. */
+typedef struct {
+  const void* pts;
+  const void* target_u;
+  const void* target_p;
+  long long n;
+  double vel_coef;
+  double p_coef;
+} fr_mse_set;
+
+int fr_epoch_workspace(const fr_plan* plan, long long n_colloc, const long long* n_sets, int n_set_count,
+                       fr_workspace* out);
+int fr_epoch_fwd_bwd(const fr_plan* plan, const void* kparams, const void* colloc, long long n_colloc,
+                     double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
+                     double* gpart, double* const* lpart_blocks, void* scratch, fr_stream_t stream);
 
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,

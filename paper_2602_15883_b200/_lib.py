@@ -62,6 +62,11 @@ class AdamArgs(C.Structure):
     ]
 
 
+class MseSet(C.Structure):
+    _fields_ = [("pts", C.c_void_p), ("target_u", C.c_void_p), ("target_p", C.c_void_p),
+                ("n", C.c_longlong), ("vel_coef", C.c_double), ("p_coef", C.c_double)]
+
+
 # name -> (restype, argtypes); every function returns int status unless noted
 _P = C.c_void_p
 _SIGS = {
@@ -72,6 +77,9 @@ _SIGS = {
     "fr_prepare_params": [_P, _P, _P, _P],
     "fr_pde_fwd_bwd": [_P, _P, _P, C.c_longlong, C.c_double, _P, _P, _P, _P],
     "fr_mse_fwd_bwd": [_P, _P, _P, _P, _P, C.c_longlong, _P, C.c_double, C.c_double, _P, _P, _P, _P],
+    "fr_epoch_workspace": [_P, C.c_longlong, C.POINTER(C.c_longlong), C.c_int, C.POINTER(Workspace)],
+    "fr_epoch_fwd_bwd": [_P, _P, _P, C.c_longlong, C.c_double, C.POINTER(MseSet), C.c_int, _P, _P,
+                         C.POINTER(C.c_void_p), _P, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
@@ -113,7 +121,7 @@ def lib():
 
 # functions that enqueue kernels (counted for the bench's gpu_launches claim)
 LAUNCHERS = frozenset({
-    "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
+    "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_jet_act_forward",
     "fr_jet_act_backward", "fr_bench_ffma",
 })

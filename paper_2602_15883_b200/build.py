@@ -19,7 +19,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflowrec_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["capi.cu", "jetmlp_pde.cu", "jetmlp_mse.cu", "jetmlp_value.cu", "jetmlp_jet.cu"]
+SOURCES = ["capi.cu"] + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet") for d in ("f32", "f64")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

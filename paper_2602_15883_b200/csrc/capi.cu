@@ -13,10 +13,16 @@
 #include "jetmlp_dispatch.cuh"
 
 namespace fr {
-int mode_entry_PDE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
-int mode_entry_MSE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
-int mode_entry_VALUE(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
-int mode_entry_JET(int, int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+#define FR_DECL(NAME) \
+  int NAME##_f32(int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int); \
+  int NAME##_f64(int, int, int, const KArgs*, int, cudaStream_t, KInfo*, int);
+FR_DECL(mode_entry_PDE)
+FR_DECL(mode_entry_MSE)
+FR_DECL(mode_entry_VALUE)
+FR_DECL(mode_entry_JET)
+#undef FR_DECL
+int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
+int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 }  // namespace fr
 
 using namespace fr;
@@ -81,9 +87,8 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
     if (arch[i] != width) return fail("hidden layers must share one width (ExpertConfig); got %d and %d", width, arch[i]);
   int wpad;
   if (width <= 16) wpad = 16;
-  else if (width <= 32) wpad = 32;
   else if (width <= 64) wpad = 64;
-  else return fail("hidden width %d > 64 is not supported by the SIMT kernels", width);
+  else return fail("hidden width %d > 64 is not supported by the fused SIMT kernels", width);
   if (!(inv_re > 0.0) || !std::isfinite(inv_re)) return fail("inv_re must be positive and finite");
 
   fr_plan* p = new fr_plan();
@@ -159,16 +164,37 @@ extern "C" int fr_plan_get_info(const fr_plan* p, fr_plan_info* out) {
 
 static int mode_call(const fr_plan* p, int mode, const KArgs* a, int grid, cudaStream_t st, KInfo* info) {
   const fr_plan_info& I = p->info;
+  const bool f32 = I.dtype == FR_F32;
+  const int act = I.act, reg = I.regime, w = I.width_pad, L = I.hidden_layers;
   int r;
   switch (mode) {
-    case FR_MODE_PDE: r = mode_entry_PDE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
-    case FR_MODE_MSE: r = mode_entry_MSE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
-    case FR_MODE_VALUE: r = mode_entry_VALUE(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
-    case FR_MODE_JET: r = mode_entry_JET(I.dtype, I.act, I.regime, I.width_pad, a, grid, st, info, I.hidden_layers); break;
+    case FR_MODE_PDE:
+      r = f32 ? mode_entry_PDE_f32(act, reg, w, a, grid, st, info, L) : mode_entry_PDE_f64(act, reg, w, a, grid, st, info, L);
+      break;
+    case FR_MODE_MSE:
+      r = f32 ? mode_entry_MSE_f32(act, reg, w, a, grid, st, info, L) : mode_entry_MSE_f64(act, reg, w, a, grid, st, info, L);
+      break;
+    case FR_MODE_VALUE:
+      r = f32 ? mode_entry_VALUE_f32(act, reg, w, a, grid, st, info, L)
+              : mode_entry_VALUE_f64(act, reg, w, a, grid, st, info, L);
+      break;
+    case FR_MODE_JET:
+      r = f32 ? mode_entry_JET_f32(act, reg, w, a, grid, st, info, L) : mode_entry_JET_f64(act, reg, w, a, grid, st, info, L);
+      break;
     default: return fail("unknown mode %d", mode);
   }
   if (r == -1) return fail("kernel variant not compiled (mode %d dtype %d act %d regime %d width %d)", mode, I.dtype, I.act, I.regime, I.width_pad);
   if (r != 0) return cuda_fail(cudaError_t(r), "jet-MLP kernel launch");
+  return 0;
+}
+
+static int epoch_call(const fr_plan* p, const EpochArgs* e, int grid, cudaStream_t st, KInfo* info) {
+  const fr_plan_info& I = p->info;
+  const int r = I.dtype == FR_F32
+                    ? epoch_entry_f32(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers)
+                    : epoch_entry_f64(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers);
+  if (r == -1) return fail("epoch kernel variant not compiled");
+  if (r != 0) return cuda_fail(cudaError_t(r), "epoch kernel launch");
   return 0;
 }
 
@@ -253,6 +279,79 @@ extern "C" int fr_mse_fwd_bwd(const fr_plan* p, const void* kparams, const void*
   if (vel_w)
     for (int c = 0; c < p->info.n_vel; ++c) a.velw[c] = vel_w[c];
   return launch_train(p, FR_MODE_MSE, a, n, stream);
+}
+
+static int epoch_info(const fr_plan* p, KInfo* ki) { return epoch_call(p, nullptr, 0, nullptr, ki); }
+
+extern "C" int fr_epoch_workspace(const fr_plan* p, long long n_colloc, const long long* n_sets, int n_set_count,
+                                  fr_workspace* out) {
+  if (!p || !out || n_set_count < 0 || n_set_count > 3 || (n_set_count && !n_sets))
+    return fail("fr_epoch_workspace: bad arguments");
+  KInfo ki{};
+  if (epoch_info(p, &ki)) return 1;
+  const int sms = p->info.num_sms > 0 ? p->info.num_sms : 148;
+  long long tiles = (n_colloc + ki.ppt - 1) / ki.ppt;
+  for (int i = 0; i < n_set_count; ++i) tiles += (n_sets[i] + ki.ppt_mse - 1) / ki.ppt_mse;
+  out->grid = int(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+  out->threads = ki.nt;
+  out->points_per_tile = ki.ppt;
+  out->jet_streams = 0;
+  out->gpart_elems = (long long)out->grid * p->info.np_pad;
+  out->lpart_elems = (long long)out->grid * 2 * (1 + n_set_count);
+  out->scratch_bytes = (long long)out->grid * ki.stash_elems * (p->info.dtype == FR_F32 ? 4 : 8);
+  out->smem_bytes = ki.smem;
+  return 0;
+}
+
+extern "C" int fr_epoch_fwd_bwd(const fr_plan* p, const void* kparams, const void* colloc, long long n_colloc,
+                                double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
+                                double* gpart, double* const* lpart_blocks, void* scratch, fr_stream_t stream) {
+  if (!p || !kparams || !colloc || n_colloc < 1 || !gpart || !lpart_blocks || !scratch || n_set_count < 0 ||
+      n_set_count > 3 || (n_set_count && !sets))
+    return fail("fr_epoch_fwd_bwd: bad arguments");
+  long long ns[3] = {0, 0, 0};
+  for (int i = 0; i < n_set_count; ++i) {
+    if (sets[i].n < 0 || (sets[i].n > 0 && (!sets[i].pts || !sets[i].target_u)))
+      return fail("fr_epoch_fwd_bwd: bad MSE set %d", i);
+    ns[i] = sets[i].n;
+  }
+  for (int i = 0; i < 1 + n_set_count; ++i)
+    if (!lpart_blocks[i]) return fail("fr_epoch_fwd_bwd: NULL loss-partial block %d", i);
+  fr_workspace ws;
+  if (fr_epoch_workspace(p, n_colloc, ns, n_set_count, &ws)) return 1;
+  KInfo ki{};
+  if (epoch_info(p, &ki)) return 1;
+  const fr_plan_info& I = p->info;
+  EpochArgs e{};
+  auto fill = [&](KArgs& a, long long n) {
+    a.kp = kparams;
+    a.gpart = gpart;
+    a.scratch = scratch;
+    a.n = n;
+    a.L = I.hidden_layers;
+    a.np_pad = I.np_pad;
+    a.stash_elems = ki.stash_elems;
+    a.inv_re = I.inv_re;
+    for (int c = 0; c < 4; ++c) a.velw[c] = 1.0;
+    if (vel_w)
+      for (int c = 0; c < I.n_vel; ++c) a.velw[c] = vel_w[c];
+  };
+  fill(e.pde, n_colloc);
+  e.pde.pts = colloc;
+  e.pde.coef = pde_coef;
+  e.pde.lpart = lpart_blocks[0];
+  e.n_mse = n_set_count;
+  for (int i = 0; i < n_set_count; ++i) {
+    fill(e.mse[i], sets[i].n);
+    e.mse[i].pts = sets[i].pts;
+    e.mse[i].tu = sets[i].target_u;
+    e.mse[i].tp = sets[i].target_p;
+    e.mse[i].has_p = sets[i].target_p != nullptr;
+    e.mse[i].coef = sets[i].vel_coef;
+    e.mse[i].pcoef = sets[i].p_coef;
+    e.mse[i].lpart = lpart_blocks[1 + i];
+  }
+  return epoch_call(p, &e, ws.grid, stream, nullptr);
 }
 
 extern "C" int fr_value_fwd(const fr_plan* p, const void* kparams, const void* pts, long long n, void* out,

@@ -10,7 +10,28 @@ struct KInfo {
   int ppt;           // points per tile
   int stash_elems;   // per-CTA stash elements (of T)
   size_t smem;       // dynamic shared memory bytes
+  int ppt_mse;       // epoch kernel: points per MSE tile
 };
+
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+
+template <class F>
+int dispatch_act_reg(int act, int reg, F&& go) {
+  if (act == ACT_TANH) {
+    if (reg == REG_STEADY2D) return go(IntC<ACT_TANH>{}, IntC<REG_STEADY2D>{});
+    if (reg == REG_UNSTEADY2D) return go(IntC<ACT_TANH>{}, IntC<REG_UNSTEADY2D>{});
+    if (reg == REG_UNSTEADY3D) return go(IntC<ACT_TANH>{}, IntC<REG_UNSTEADY3D>{});
+  }
+  if (act == ACT_SIN) {
+    if (reg == REG_STEADY2D) return go(IntC<ACT_SIN>{}, IntC<REG_STEADY2D>{});
+    if (reg == REG_UNSTEADY2D) return go(IntC<ACT_SIN>{}, IntC<REG_UNSTEADY2D>{});
+    if (reg == REG_UNSTEADY3D) return go(IntC<ACT_SIN>{}, IntC<REG_UNSTEADY3D>{});
+  }
+  return -1;
+}
 
 template <typename T, int ACT, int MODE, int REG, int W>
 int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
@@ -36,40 +57,68 @@ int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
   return int(cudaGetLastError());
 }
 
-// returns -1 when the combination is not compiled in
-template <int MODE>
-int dispatch_mode(int dtype, int act, int reg, int w, const KArgs* a, int grid, cudaStream_t st,
-                  KInfo* info, int L) {
-#define FR_CASE_W(T, ACT, REG)                                                        \
-  if (w == 16) return run_mode<T, ACT, MODE, REG, 16>(a, grid, st, info, L);          \
-  if (w == 32) return run_mode<T, ACT, MODE, REG, 32>(a, grid, st, info, L);          \
-  if (w == 64) return run_mode<T, ACT, MODE, REG, 64>(a, grid, st, info, L);          \
-  return -1;
-#define FR_CASE_REG(T, ACT)                                   \
-  switch (reg) {                                              \
-    case REG_STEADY2D: { FR_CASE_W(T, ACT, REG_STEADY2D) }     \
-    case REG_UNSTEADY2D: { FR_CASE_W(T, ACT, REG_UNSTEADY2D) } \
-    case REG_UNSTEADY3D: { FR_CASE_W(T, ACT, REG_UNSTEADY3D) } \
-    default: return -1;                                       \
+template <typename T, int ACT, int REG, int W>
+int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
+  using CP = JetCfg<T, ACT, MODE_PDE, REG, W>;
+  using CM = JetCfg<T, ACT, MODE_MSE, REG, W, CP::NT>;
+  const size_t smem = CP::smem_bytes(L) > CM::smem_bytes(L) ? CP::smem_bytes(L) : CM::smem_bytes(L);
+  const int sp = CP::stash_per_thread(L) > CM::stash_per_thread(L) ? CP::stash_per_thread(L) : CM::stash_per_thread(L);
+  if (info) {
+    info->nt = CP::NT;
+    info->ppt = CP::PPT;
+    info->ppt_mse = CM::PPT;
+    info->stash_elems = CP::NT * sp;
+    info->smem = smem;
   }
-#define FR_CASE_ACT(T)                             \
-  if (act == ACT_TANH) { FR_CASE_REG(T, ACT_TANH) } \
-  if (act == ACT_SIN) { FR_CASE_REG(T, ACT_SIN) }   \
-  return -1;
-  if (dtype == 0) { FR_CASE_ACT(float) }
-  if (dtype == 1) { FR_CASE_ACT(double) }
-  return -1;
-#undef FR_CASE_ACT
-#undef FR_CASE_REG
-#undef FR_CASE_W
+  if (!e) return 0;
+  auto k = jetmlp_epoch_kernel<T, ACT, REG, W>;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return int(err);
+    smem_set = smem;
+  }
+  k<<<grid, CP::NT, smem, st>>>(*e);
+  return int(cudaGetLastError());
+}
+
+// returns -1 when the combination is not compiled in
+template <int MODE, typename T>
+int dispatch_mode_t(int act, int reg, int w, const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
+  auto go = [&](auto act_c, auto reg_c) -> int {
+    constexpr int ACT = decltype(act_c)::value, REG = decltype(reg_c)::value;
+    if (w == 16) return run_mode<T, ACT, MODE, REG, 16>(a, grid, st, info, L);
+    if (w == 64) return run_mode<T, ACT, MODE, REG, 64>(a, grid, st, info, L);
+    return -1;
+  };
+  return dispatch_act_reg(act, reg, go);
+}
+
+template <typename T>
+int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
+  auto go = [&](auto act_c, auto reg_c) -> int {
+    constexpr int ACT = decltype(act_c)::value, REG = decltype(reg_c)::value;
+    if (w == 16) return run_epoch<T, ACT, REG, 16>(e, grid, st, info, L);
+    if (w == 64) return run_epoch<T, ACT, REG, 64>(e, grid, st, info, L);
+    return -1;
+  };
+  return dispatch_act_reg(act, reg, go);
 }
 
 }  // namespace fr
 
-#define FR_DEFINE_MODE_ENTRY(M)                                                                  \
-  namespace fr {                                                                                 \
-  int mode_entry_##M(int dtype, int act, int reg, int w, const KArgs* a, int grid, cudaStream_t st, \
-                     KInfo* info, int L) {                                                       \
-    return dispatch_mode<MODE_##M>(dtype, act, reg, w, a, grid, st, info, L);                    \
-  }                                                                                              \
+// one translation unit per (mode, dtype) keeps the parallel build short
+#define FR_DEFINE_MODE_ENTRY(M, T, TAG)                                                                \
+  namespace fr {                                                                                      \
+  int mode_entry_##M##_##TAG(int act, int reg, int w, const KArgs* a, int grid, cudaStream_t st,       \
+                             KInfo* info, int L) {                                                    \
+    return dispatch_mode_t<MODE_##M, T>(act, reg, w, a, grid, st, info, L);                           \
+  }                                                                                                   \
+  }
+#define FR_DEFINE_EPOCH_ENTRY(T, TAG)                                                                  \
+  namespace fr {                                                                                      \
+  int epoch_entry_##TAG(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st,        \
+                        KInfo* info, int L) {                                                         \
+    return dispatch_epoch_t<T>(act, reg, w, e, grid, st, info, L);                                    \
+  }                                                                                                   \
   }

@@ -98,7 +98,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------------------
 // compile-time configuration
 // ---------------------------------------------------------------------------
-template <typename T, int ACT, int MODE, int REG, int W>
+template <typename T, int ACT, int MODE, int REG, int W, int NT_ = 0>
 struct JetCfg {
   using R = Regime<REG>;
   using St = Streams<MODE, REG>;
@@ -108,7 +108,8 @@ struct JetCfg {
   static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE);
   // 12 warps per SM where the FP32 tile buffers still fit (W = 64, <= 6 streams);
   // otherwise 8 (FP32) or 4 (FP64 parity build)
-  static constexpr int NT = sizeof(T) == 4 ? ((W == 64 && St::RPT <= 6) ? 384 : 256) : 128;
+  static constexpr int NT_DEFAULT = sizeof(T) == 4 ? ((W == 64 && St::RPT <= 6) ? 384 : 256) : 128;
+  static constexpr int NT = NT_ ? NT_ : NT_DEFAULT;
   static constexpr int G = W / 8;          // unit groups of 8 per row group
   static constexpr int NRG = NT / G;       // row groups
   static constexpr int ROWS = NRG * RPT;   // rows per tile
@@ -244,16 +245,19 @@ __device__ __forceinline__ void load_block(T (&v)[RPT][8], const T* __restrict__
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <typename T, int ACT, int MODE, int REG, int W>
-__global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_kernel(KArgs a) {
-  using C = JetCfg<T, ACT, MODE, REG, W>;
+// Processes tiles t0, t0 + tstride, ... of one dataset with this CTA.  Gradient
+// contributions are red.add-ed into gp_row (zeroed first when zero_partials);
+// the CTA's loss sums are written to lpart_row[0..1].
+template <typename T, int ACT, int MODE, int REG, int W, int NT_>
+__device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_raw, long long t0, long long tstride,
+                                          bool zero_partials, double* gp_row, double* lpart_row) {
+  using C = JetCfg<T, ACT, MODE, REG, W, NT_>;
   constexpr int NT = C::NT, G = C::G, RPT = C::RPT, ROWS = C::ROWS, PPT = C::PPT;
   constexpr int DIN = C::DIN, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
   constexpr int NG = C::NG, NL = C::NL, LAP0 = C::LAP0, RS4 = C::RS4;
   constexpr int NST0 = C::NST0, NSTH = C::NSTH, PP = C::PP;
   constexpr bool JET = C::JET, BWD = C::BWD;
 
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.L;
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* Xs = sm;                      sm += C::al(C::XELEMS);
@@ -291,8 +295,9 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
 
   double* gp = nullptr;
   if constexpr (BWD) {
-    gp = a.gpart + size_t(blockIdx.x) * a.np_pad;
-    for (int i = tid; i < a.np_pad; i += NT) gp[i] = 0.0;
+    gp = gp_row;
+    if (zero_partials)
+      for (int i = tid; i < a.np_pad; i += NT) gp[i] = 0.0;
   }
   T* stash = static_cast<T*>(a.scratch) + size_t(blockIdx.x) * a.stash_elems;
   auto st_idx = [&](int layer, int q) { return (C::stash_layer_base(layer) + q) * NT + tid; };
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
   __syncthreads();
 
   const long long ntiles = (n + PPT - 1) / PPT;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (long long tile = t0; tile < ntiles; tile += tstride) {
     const long long p0 = tile * PPT;
     {
       const T* pts = static_cast<const T*>(a.pts) + p0 * DIN;
@@ -842,8 +847,8 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
     }
   }
 
+  cp_async_wait_all();
   if constexpr (BWD) {
-    cp_async_wait_all();
     red[tid] = lacc0;
     red[NT + tid] = lacc1;
     __syncthreads();
@@ -853,9 +858,46 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
         s0 += red[i];
         s1 += red[NT + i];
       }
-      a.lpart[2 * blockIdx.x] = s0;
-      a.lpart[2 * blockIdx.x + 1] = s1;
+      lpart_row[0] = s0;
+      lpart_row[1] = s1;
     }
+  }
+  __syncthreads();  // shared memory is reused by the caller's next dataset
+}
+
+// one dataset per launch
+template <typename T, int ACT, int MODE, int REG, int W>
+__global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_kernel(KArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT = JetCfg<T, ACT, MODE, REG, W>::NT;
+  run_tiles<T, ACT, MODE, REG, W, NT>(a, smem_raw, blockIdx.x, gridDim.x, true,
+                                      a.gpart ? a.gpart + size_t(blockIdx.x) * a.np_pad : nullptr,
+                                      a.lpart ? a.lpart + 2 * blockIdx.x : nullptr);
+}
+
+// A whole epoch's loss heads in one persistent launch: every CTA first walks its
+// static share of PDE tiles, then MSE tiles (obs, ghost-spatial, ghost-temporal)
+// dealt out from the last CTA backwards, i.e. to the CTAs that got one PDE tile
+// fewer.  Assignment is static, so the per-CTA partial sums -- and the reduced
+// loss and gradient -- are identical on every run.
+struct EpochArgs {
+  KArgs pde;
+  KArgs mse[3];
+  int n_mse;
+};
+
+template <typename T, int ACT, int REG, int W>
+__global__ void __launch_bounds__(JetCfg<T, ACT, MODE_PDE, REG, W>::NT, 1) jetmlp_epoch_kernel(EpochArgs e) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT = JetCfg<T, ACT, MODE_PDE, REG, W>::NT;
+  const long long G = gridDim.x, c = blockIdx.x;
+  double* gp = e.pde.gpart + size_t(c) * e.pde.np_pad;
+  run_tiles<T, ACT, MODE_PDE, REG, W, NT>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c);
+  long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W>::PPT;
+  for (int d = 0; d < e.n_mse; ++d) {
+    const long long t0 = (((G - 1 - c) - offset) % G + G) % G;
+    run_tiles<T, ACT, MODE_MSE, REG, W, NT>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c);
+    offset += (e.mse[d].n + JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT;
   }
 }
 

@@ -10,8 +10,8 @@ Mirrors pkg/src/flowrec/runtime/driver.py:43-283.  Backends:
                      exchange, one without), so an epoch costs one graph launch.
   "distributed"      this process is one rank of an initialised
                      torch.distributed group (one process per GPU, launched by
-                     torchrun); ghost messages move by NCCL point-to-point,
-                     overlapped with the interior (obs + PDE) kernels.
+                     torchrun); ghost messages move by NCCL point-to-point
+                     straight into the receiver's ghost-target buffers.
   "process"          spawns one process per rank, one GPU each (needs at least
                      as many GPUs as ranks) and runs "distributed" in each.
 
@@ -239,19 +239,20 @@ class DistributedTrainer:
         self.recv_bufs = {gi: w.objective.target_slice(gi) for _, gi, _ in self.recvs}
 
     def epoch(self, e):
+        """Exchange (if due) then the fused epoch.  The persistent epoch kernel
+        occupies every SM, so NCCL's P2P kernels could not run underneath it;
+        the (latency-bound, ~10-30 us) exchange is therefore issued first and
+        the epoch kernel consumes the received ghost targets directly."""
         w = self.worker
         exchange = e % self.plan.train_config.comm_interval == 0
-        works = []
         if exchange:
             w.produce()
             for k, _ in enumerate(self.sends):
                 w.pack_edge(k, *self.send_bufs[k])
-            works = post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs)
+            for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                wk.wait()  # orders the compute stream after the transfers (no host sync)
             w.objective.mark_targets_set()
-        w.enqueue_epoch(part="interior")   # overlaps the NCCL transfers
-        for wk in works:
-            wk.wait()                      # compute stream waits for the receives
-        w.enqueue_epoch(part="rest")
+        w.enqueue_epoch()
         w.epochs_done += 1
         if exchange:
             w.exchange_log.append((e, sorted(w.expected_messages)))

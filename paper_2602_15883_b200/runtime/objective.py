@@ -75,31 +75,46 @@ class DeviceObjective:
             }
         self.targets_set = {k: False for k in self.ghost}
 
-        # launch list and workspaces: gradient / loss partial rows are laid out
-        # contiguously in dataset order so one fixed-order reduction covers all
-        self.segments = []
-        rows = 0
-        scratch = 0
-        seg_rows = [0, 0, 0, 0]
-        plan_segs = [(SEG_OBS, X.MODE_MSE, self.n_obs), (SEG_PDE, X.MODE_PDE, self.n_colloc)]
-        plan_segs += [(SEG_GS if k == "spatial" else SEG_GT, X.MODE_MSE, counts[k]) for k in KINDS]
-        for seg, mode, n in plan_segs:
-            if n == 0:
-                continue
-            ws = plan.workspace(mode, n)
-            self.segments.append((seg, mode, n, rows, ws))
-            seg_rows[seg] = ws.grid
-            rows += ws.grid
-            scratch = max(scratch, ws.scratch_bytes)
-        self.total_rows = rows
-        self.seg_rows = (ctypes.c_int * 4)(*seg_rows)
+        # one persistent launch per epoch covers every loss head (obs, PDE,
+        # ghost-spatial, ghost-temporal); loss-partial blocks are packed in the
+        # reference's dataset order so the optimiser kernel can reduce them
+        self.set_order = []  # (segment id, kind or None) of the MSE sets, in launch order
+        if self.n_obs:
+            self.set_order.append((SEG_OBS, None))
+        for kind, seg in (("spatial", SEG_GS), ("temporal", SEG_GT)):
+            if counts[kind]:
+                self.set_order.append((seg, kind))
+        n_sets = (ctypes.c_longlong * 3)(*([self._set_n(sg, k) for sg, k in self.set_order] + [0] * 3)[:3])
+        ws = X.Workspace()
+        X.call("fr_epoch_workspace", plan.h, self.n_colloc, n_sets, len(self.set_order), ctypes.byref(ws))
+        self.ws = ws
+        self.grid = ws.grid
+        present = [SEG_OBS] if self.n_obs else []
+        present += [SEG_PDE] + [sg for sg, k in self.set_order if k is not None]
+        self.seg_rows = (ctypes.c_int * 4)(*[ws.grid if sg in present else 0 for sg in range(4)])
+        self.total_rows = ws.grid
         npad = plan.info.np_pad
-        self.gpart = torch.empty(max(rows, 1) * npad, dtype=torch.float64, device=dev)
-        self.lpart = torch.empty(max(rows, 1) * 2, dtype=torch.float64, device=dev)
-        self.scratch = torch.empty(max(scratch, 16), dtype=torch.uint8, device=dev)
+        self.gpart = torch.empty(ws.grid * npad, dtype=torch.float64, device=dev)
+        self.lpart = torch.zeros(len(present) * ws.grid * 2, dtype=torch.float64, device=dev)
+        block = {sg: self.lpart.data_ptr() + 8 * 2 * ws.grid * i for i, sg in enumerate(present)}
+        self.lpart_blocks = (ctypes.c_void_p * 4)(block[SEG_PDE], *[block[sg] for sg, _ in self.set_order])
+        self.scratch = torch.empty(max(ws.scratch_bytes, 16), dtype=torch.uint8, device=dev)
+        self.sets = (X.MseSet * 3)()
+        for i, (sg, kind) in enumerate(self.set_order):
+            st = self.sets[i]
+            if kind is None:
+                st.pts, st.target_u, st.target_p = self.obs_pts.data_ptr(), self.obs_vel.data_ptr(), None
+                st.n, st.vel_coef, st.p_coef = self.n_obs, weights.obs / self.n_obs, 0.0
+            else:
+                g = self.ghost[kind]
+                st.pts, st.target_u, st.target_p = g["pts"].data_ptr(), g["tu"].data_ptr(), g["tp"].data_ptr()
+                st.n, st.vel_coef, st.p_coef = counts[kind], g["vel_coef"], g["p_coef"]
         self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
         self.norm_parts = torch.zeros(X.lib().fr_reduce_grad_parts(plan.h), dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+
+    def _set_n(self, seg, kind):
+        return self.n_obs if kind is None else self.n_ghost[kind]
 
     # -- ghost targets --------------------------------------------------------
     def target_slice(self, gi):
@@ -135,44 +150,22 @@ class DeviceObjective:
                     n_ghost_time=float(self.n_ghost["temporal"]), w_obs=w.obs, w_pde=w.pde,
                     w_ghost_u=w.ghost_u, w_ghost_p_space=w.ghost_p_space, w_ghost_p_time=w.ghost_p_time)
 
-    def enqueue(self, kparams, stream=None, part="all", with_sums=True):
-        """Launch the epoch's loss/gradient kernels and reductions (no sync).
-
-        part: "all"; "interior" = obs + PDE heads (independent of the ghost
-        exchange); "rest" = ghost heads + fixed-order reductions.  with_sums
-        also reduces the loss partials into `sums` (the training loop leaves
-        that to the optimiser kernel, which reads the partials directly)."""
-        interior = part in ("all", "interior")
-        rest = part in ("all", "rest")
-        if rest:
-            for kind in self.ghost:
-                if not self.targets_set[kind]:
-                    raise RuntimeError(f"{kind} ghost targets were never set; run an exchange first")
-        plan, npad = self.plan, self.plan.info.np_pad
+    def enqueue(self, kparams, stream=None, with_sums=True):
+        """Launch the epoch's loss/gradient kernel and the fixed-order gradient
+        reduction (no sync).  with_sums also reduces the loss partials into
+        `sums` (the training loop leaves that to the optimiser kernel)."""
+        for kind in self.ghost:
+            if not self.targets_set[kind]:
+                raise RuntimeError(f"{kind} ghost targets were never set; run an exchange first")
+        plan = self.plan
         st = X.stream_ptr(stream)
-        kp = X.ptr(kparams)
-        sc = X.ptr(self.scratch)
-        for seg, mode, n, row, ws in self.segments:
-            is_ghost = seg in (SEG_GS, SEG_GT)
-            if (is_ghost and not rest) or (not is_ghost and not interior):
-                continue
-            gp = self.gpart.data_ptr() + 8 * row * npad
-            lp = self.lpart.data_ptr() + 8 * 2 * row
-            if mode == X.MODE_PDE:
-                X.call("fr_pde_fwd_bwd", plan.h, kp, X.ptr(self.col_pts), n,
-                       self.weights.pde / self.n_colloc, gp, lp, sc, st)
-            elif seg == SEG_OBS:
-                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(self.obs_pts), X.ptr(self.obs_vel), None, n,
-                       self.vel_w, self.weights.obs / self.n_obs, 0.0, gp, lp, sc, st)
-            else:
-                g = self.ghost["spatial" if seg == SEG_GS else "temporal"]
-                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(g["pts"]), X.ptr(g["tu"]), X.ptr(g["tp"]), n,
-                       self.vel_w, g["vel_coef"], g["p_coef"], gp, lp, sc, st)
-        if rest:
-            X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
-                   X.ptr(self.norm_parts), st)
-            if with_sums:
-                X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
+        X.call("fr_epoch_fwd_bwd", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
+               self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
+               X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch), st)
+        X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
+               X.ptr(self.norm_parts), st)
+        if with_sums:
+            X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
 
     def parts_from_sums(self, sums):
         """Unweighted LossParts from the reduced sums (objective.py:183-191)."""
