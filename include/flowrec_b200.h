@@ -63,6 +63,8 @@ typedef struct {
   long long lpart_elems;   /* doubles: grid * 2 */
   long long scratch_bytes; /* per-call stash workspace */
   size_t smem_bytes;
+  int loss_rows;           /* rows of 2 doubles in lpart (== grid for the fused kernels) */
+  int wide;                /* 1: layer-wise wide kernels (hidden width > 64) */
 } fr_workspace;
 
 /* Plan: validated network + regime description (replaces per-bind checks). */

@@ -19,7 +19,8 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflowrec_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["capi.cu"] + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet") for d in ("f32", "f64")]
+SOURCES = (["capi.cu", "wide_f32.cu", "wide_f64.cu"]
+           + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet") for d in ("f32", "f64")])
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

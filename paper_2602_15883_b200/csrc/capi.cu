@@ -11,6 +11,7 @@
 
 #include "../../include/flowrec_b200.h"
 #include "jetmlp_dispatch.cuh"
+#include "wide_kernel.cuh"
 
 namespace fr {
 #define FR_DECL(NAME) \
@@ -22,6 +23,8 @@ FR_DECL(mode_entry_VALUE)
 FR_DECL(mode_entry_JET)
 #undef FR_DECL
 int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
+int wide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
+int wide_entry_f64(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 }  // namespace fr
 
@@ -85,10 +88,13 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   const int width = arch[1];
   for (int i = 1; i < n_arch - 1; ++i)
     if (arch[i] != width) return fail("hidden layers must share one width (ExpertConfig); got %d and %d", width, arch[i]);
+  // widths <= 64 run the fused per-tile kernels; wider experts the layer-wise
+  // kernels, padded to whole 64-unit blocks (zero weights: exact)
   int wpad;
   if (width <= 16) wpad = 16;
   else if (width <= 64) wpad = 64;
-  else return fail("hidden width %d > 64 is not supported by the fused SIMT kernels", width);
+  else if (width <= 1024) wpad = (width + 63) / 64 * 64;
+  else return fail("hidden width %d > 1024 is not supported", width);
   if (!(inv_re > 0.0) || !std::isfinite(inv_re)) return fail("inv_re must be positive and finite");
 
   fr_plan* p = new fr_plan();
@@ -198,9 +204,57 @@ static int epoch_call(const fr_plan* p, const EpochArgs* e, int grid, cudaStream
   return 0;
 }
 
+constexpr int WIDE_KS = 32;  // gradient-partial rows (row splits) of the wide kernels
+
+static bool is_wide(const fr_plan* p) { return p->info.width_pad > 64; }
+
+static int wide_call(const fr_plan* p, int mode, const WArgs* a, cudaStream_t st, WInfo* wi) {
+  const fr_plan_info& I = p->info;
+  const int r = I.dtype == FR_F32 ? wide_entry_f32(mode, I.act, I.regime, a, WIDE_KS, st, wi)
+                                  : wide_entry_f64(mode, I.act, I.regime, a, WIDE_KS, st, wi);
+  if (r == -1) return fail("wide kernel variant not compiled");
+  if (r != 0) return cuda_fail(cudaError_t(r), "wide kernel launch");
+  return 0;
+}
+
+struct WideSizes {
+  long long ntiles, act, stash, ybar, total;  // elements of T
+};
+static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WInfo* wi) {
+  if (wide_call(p, mode, nullptr, nullptr, wi)) return 1;
+  const fr_plan_info& I = p->info;
+  const long long L = I.hidden_layers, WP = I.width_pad;
+  z->ntiles = (n + wi->ppt - 1) / wi->ppt;
+  z->act = L * z->ntiles * WP * wi->rows;
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  z->stash = bwd ? L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt : 0;
+  z->ybar = bwd ? z->ntiles * wi->rows * I.n_out : 0;
+  auto al = [](long long e) { return (e + 63) / 64 * 64; };
+  z->total = al(z->act) + (bwd ? al(z->act) : 0) + al(z->stash) + al(z->ybar);
+  return 0;
+}
+
 extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_workspace* out) {
   if (!p || !out) return fail("fr_plan_workspace: NULL argument");
   if (n < 0) return fail("negative point count");
+  if (is_wide(p)) {
+    WideSizes z;
+    WInfo wi{};
+    if (wide_sizes(p, mode, n, &z, &wi)) return 1;
+    const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+    const size_t esz = p->info.dtype == FR_F32 ? 4 : 8;
+    out->grid = WIDE_KS;
+    out->threads = wi.nt;
+    out->points_per_tile = wi.ppt;
+    out->jet_streams = 1 + 2 * p->info.n_in;
+    out->gpart_elems = bwd ? (long long)WIDE_KS * p->info.np_pad : 0;
+    out->lpart_elems = bwd ? z.ntiles * 2 : 0;
+    out->loss_rows = bwd ? int(z.ntiles) : 0;
+    out->scratch_bytes = z.total * (long long)esz;
+    out->smem_bytes = 0;
+    out->wide = 1;
+    return 0;
+  }
   KInfo ki{};
   if (mode_call(p, mode, nullptr, 0, nullptr, &ki)) return 1;
   const fr_plan_info& I = p->info;
@@ -216,7 +270,49 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
   const size_t esz = I.dtype == FR_F32 ? 4 : 8;
   out->scratch_bytes = bwd ? (long long)out->grid * ki.stash_elems * (long long)esz : 0;
   out->smem_bytes = ki.smem;
+  out->loss_rows = bwd ? out->grid : 0;
+  out->wide = 0;
   return 0;
+}
+
+// Layer-wise path: fill WArgs over a caller scratch buffer (or a stream-ordered
+// allocation for the forward-only entry points, which take no workspace) and
+// launch the sequence.
+static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* scratch, cudaStream_t st) {
+  const fr_plan_info& I = p->info;
+  WideSizes z;
+  WInfo wi{};
+  if (wide_sizes(p, mode, n, &z, &wi)) return 1;
+  if (n == 0) return 0;
+  const size_t esz = I.dtype == FR_F32 ? 4 : 8;
+  void* owned = nullptr;
+  if (!scratch) {
+    FR_CUDA(cudaMallocAsync(&owned, size_t(z.total) * esz, st), "wide workspace allocation");
+    scratch = owned;
+  }
+  auto al = [](long long e) { return (e + 63) / 64 * 64; };
+  char* base = static_cast<char*>(scratch);
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  a.act = base;
+  base += al(z.act) * esz;
+  if (bwd) {
+    a.adj = base;
+    base += al(z.act) * esz;
+  }
+  a.stash = base;
+  base += al(z.stash) * esz;
+  a.ybar = base;
+  a.n = n;
+  a.ntiles = int(z.ntiles);
+  a.L = I.hidden_layers;
+  a.WP = I.width_pad;
+  a.np_pad = I.np_pad;
+  a.ks_rows = WIDE_KS;
+  a.inv_re = I.inv_re;
+  if (bwd) FR_CUDA(cudaMemsetAsync(a.gpart, 0, sizeof(double) * size_t(WIDE_KS) * I.np_pad, st), "gpart zero");
+  const int r = wide_call(p, mode, &a, st, nullptr);
+  if (owned) cudaFreeAsync(owned, st);
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -241,6 +337,14 @@ extern "C" int fr_prepare_params(const fr_plan* p, const double* flat, void* kpa
 }
 
 static int launch_train(const fr_plan* p, int mode, KArgs& a, long long n, cudaStream_t st) {
+  if (is_wide(p)) {
+    WArgs w{};
+    w.kp = a.kp; w.pts = a.pts; w.tu = a.tu; w.tp = a.tp; w.out = a.out;
+    w.gpart = a.gpart; w.lpart = a.lpart;
+    w.coef = a.coef; w.pcoef = a.pcoef; w.has_p = a.has_p;
+    for (int c = 0; c < 4; ++c) w.velw[c] = a.velw[c];
+    return launch_wide(p, mode, w, n, a.scratch, st);
+  }
   fr_workspace ws;
   if (fr_plan_workspace(p, mode, n, &ws)) return 1;
   a.n = n;
@@ -281,7 +385,10 @@ extern "C" int fr_mse_fwd_bwd(const fr_plan* p, const void* kparams, const void*
   return launch_train(p, FR_MODE_MSE, a, n, stream);
 }
 
-static int epoch_info(const fr_plan* p, KInfo* ki) { return epoch_call(p, nullptr, 0, nullptr, ki); }
+static int epoch_info(const fr_plan* p, KInfo* ki) {
+  if (is_wide(p)) return fail("the fused epoch kernel needs hidden width <= 64 (use the per-dataset entry points)");
+  return epoch_call(p, nullptr, 0, nullptr, ki);
+}
 
 extern "C" int fr_epoch_workspace(const fr_plan* p, long long n_colloc, const long long* n_sets, int n_set_count,
                                   fr_workspace* out) {

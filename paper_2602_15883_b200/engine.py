@@ -142,7 +142,7 @@ def _train_call(plan, mode, n, launch):
     grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
     X.call("fr_reduce_grad", plan.h, X.ptr(gpart), ws.grid, X.ptr(grad), 0, None, X.stream_ptr())
     sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    rows = (C.c_int * 1)(ws.grid)
+    rows = (C.c_int * 1)(ws.loss_rows)
     X.call("fr_reduce_loss", X.ptr(lpart), rows, 1, X.ptr(sums), X.stream_ptr())
     s = sums.cpu().numpy()
     return float(s[0]), float(s[1]), grad.cpu().numpy()

@@ -84,6 +84,10 @@ class DeviceObjective:
         for kind, seg in (("spatial", SEG_GS), ("temporal", SEG_GT)):
             if counts[kind]:
                 self.set_order.append((seg, kind))
+        self.wide = plan.info.width_pad > 64
+        if self.wide:
+            self._init_wide(plan, counts, weights, dev)
+            return
         n_sets = (ctypes.c_longlong * 3)(*([self._set_n(sg, k) for sg, k in self.set_order] + [0] * 3)[:3])
         ws = X.Workspace()
         X.call("fr_epoch_workspace", plan.h, self.n_colloc, n_sets, len(self.set_order), ctypes.byref(ws))
@@ -112,6 +116,50 @@ class DeviceObjective:
         self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
         self.norm_parts = torch.zeros(X.lib().fr_reduce_grad_parts(plan.h), dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+
+    def _init_wide(self, plan, counts, weights, dev):
+        """Wide experts (hidden width > 64): one layer-wise launch sequence per
+        dataset, each writing its own block of gradient / loss partial rows."""
+        npad = plan.info.np_pad
+        launches = [(SEG_PDE, X.MODE_PDE, None)] + [(sg, X.MODE_MSE, k) for sg, k in self.set_order]
+        launches.sort(key=lambda t: t[0])  # reference order: obs, pde, ghost-spatial, ghost-temporal
+        self.wide_launches = []
+        grow = lrow = 0
+        scratch = 0
+        seg_rows = [0, 0, 0, 0]
+        for sg, mode, kind in launches:
+            n = self.n_colloc if mode == X.MODE_PDE else self._set_n(sg, kind)
+            ws = plan.workspace(mode, n)
+            self.wide_launches.append((sg, mode, kind, n, grow, lrow))
+            seg_rows[sg] = ws.loss_rows
+            grow += ws.grid
+            lrow += ws.loss_rows
+            scratch = max(scratch, ws.scratch_bytes)
+        self.total_rows = grow
+        self.seg_rows = (ctypes.c_int * 4)(*seg_rows)
+        self.gpart = torch.zeros(grow * npad, dtype=torch.float64, device=dev)
+        self.lpart = torch.zeros(max(lrow, 1) * 2, dtype=torch.float64, device=dev)
+        self.scratch = torch.empty(max(scratch, 16), dtype=torch.uint8, device=dev)
+        self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
+        self.norm_parts = torch.zeros(X.lib().fr_reduce_grad_parts(plan.h), dtype=torch.float64, device=dev)
+        self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+
+    def _enqueue_wide(self, kparams, st):
+        plan, npad = self.plan, self.plan.info.np_pad
+        kp, sc = X.ptr(kparams), X.ptr(self.scratch)
+        for sg, mode, kind, n, grow, lrow in self.wide_launches:
+            gp = self.gpart.data_ptr() + 8 * grow * npad
+            lp = self.lpart.data_ptr() + 16 * lrow
+            if mode == X.MODE_PDE:
+                X.call("fr_pde_fwd_bwd", plan.h, kp, X.ptr(self.col_pts), n, self.weights.pde / self.n_colloc,
+                       gp, lp, sc, st)
+            elif kind is None:
+                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(self.obs_pts), X.ptr(self.obs_vel), None, n,
+                       self.vel_w, self.weights.obs / self.n_obs, 0.0, gp, lp, sc, st)
+            else:
+                g = self.ghost[kind]
+                X.call("fr_mse_fwd_bwd", plan.h, kp, X.ptr(g["pts"]), X.ptr(g["tu"]), X.ptr(g["tp"]), n,
+                       self.vel_w, g["vel_coef"], g["p_coef"], gp, lp, sc, st)
 
     def _set_n(self, seg, kind):
         return self.n_obs if kind is None else self.n_ghost[kind]
@@ -159,9 +207,12 @@ class DeviceObjective:
                 raise RuntimeError(f"{kind} ghost targets were never set; run an exchange first")
         plan = self.plan
         st = X.stream_ptr(stream)
-        X.call("fr_epoch_fwd_bwd", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
-               self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
-               X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch), st)
+        if self.wide:
+            self._enqueue_wide(kparams, st)
+        else:
+            X.call("fr_epoch_fwd_bwd", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
+                   self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
+                   X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch), st)
         X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
                X.ptr(self.norm_parts), st)
         if with_sums:

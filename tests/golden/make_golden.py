@@ -120,6 +120,9 @@ def main():
         ("steady2d", [2, 16, 16, 3], "tanh", 40.0),
         ("unsteady3d", [4, 16, 16, 4], "sin", 300.0),
         ("unsteady2d", [3, 64, 64, 64, 64, 3], "tanh", 100.0),
+        ("unsteady2d", [3, 150, 150, 150, 3], "sin", 100.0),   # wide (layer-wise kernels)
+        ("unsteady3d", [4, 200, 200, 4], "sin", 300.0),
+        ("steady2d", [2, 256, 256, 3], "tanh", 40.0),
     ]
     for i, (kind, arch, act, re) in enumerate(tape_cases):
         regime = FlowRegime(kind, re)
@@ -194,7 +197,6 @@ def main():
         gr = rng.normal(size=n) * (10.0 if k == 2 else 1.0)
         seq.append(gr.copy())
         adam_step(p, gr, st, lr=1e-2 * (0.5 ** k), clip_norm=3.0)
-    out["adam/p0"] = np.random.default_rng(0).normal(size=n)  # placeholder re-derived below
     rng2 = np.random.default_rng(999)
     p0 = rng2.normal(size=n)
     p = p0.copy()

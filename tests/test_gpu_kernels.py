@@ -34,7 +34,7 @@ def _case(golden, i):
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_jet_forward(golden, i, dtype):
     from paper_2602_15883_b200 import engine
 
@@ -52,7 +52,7 @@ def test_jet_forward(golden, i, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_pde_loss_and_gradient(golden, i, dtype):
     from paper_2602_15883_b200 import engine
 
@@ -66,7 +66,7 @@ def test_pde_loss_and_gradient(golden, i, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_mse_loss_and_gradient(golden, i, dtype):
     from paper_2602_15883_b200 import engine
 

@@ -120,3 +120,28 @@ def test_drop_in_worker_protocol(golden):
     for r, w in workers.items():
         assert rel_l2(w.flat.cpu().numpy(), ref.params[r].flat) < 1e-6
         assert max_rel(np.array(w.history)[:, 1:6], ref.history[r][:, 1:6]) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_wide_expert_training_matches_oracle(dtype):
+    """Hidden width > 64 runs the layer-wise kernels: a (1,1)x2 temporal split
+    with [3, 96x2, 3] sin experts (two masters, anchor-normalised temporal
+    messages) against the float64 oracle's serial loop."""
+    from cases import oracle_ranks
+    from oracle import flowrec_oracle as O
+    from paper_2602_15883_b200 import config as fconfig
+    from paper_2602_15883_b200.runtime import TrainConfig, build_plan, train
+
+    pb = fconfig.cylinder2d_problem(n_pde=3000, n_ghost=60, per_snapshot=12, grid_nx=9, snapshots=10,
+                                    hidden_layers=2, width=96, activation="sin", counts=(1, 1), time_splits=2)
+    tc = TrainConfig(epochs=3, batch_size=500, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor,
+                     lr_factor=0.5, lr_interval=2, seed=0)
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
+    res = train(plan, backend="serial", dtype=dtype)
+    ranks = oracle_ranks(plan)
+    hist = O.train_serial(ranks, pb.expert_config.arch, "sin", "unsteady2d", 100.0, tc.epochs, tc.lr,
+                          tc.comm_interval, tc.clip_norm, tc.anchor)
+    tol_h, tol_p = (1e-9, 1e-11) if dtype == "float64" else (F32_HIST, F32_PARAMS)
+    for r in ranks:
+        assert max_rel(res.history[r][:, 1:6], hist[r][:, 1:6]) < tol_h, (r, res.history[r], hist[r])
+        assert rel_l2(res.params[r].flat, ranks[r]["flat"]) < tol_p

@@ -19,7 +19,7 @@ def tape_case(golden, i):
     return t, arch, kind, re, act, meta
 
 
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_oracle_jets_match_reference(golden, i):
     t, arch, kind, re, act, _ = tape_case(golden, i)
     Y, _ = O.jet_forward(golden[f"{t}/params"], arch, act, golden[f"{t}/pts"])
@@ -30,7 +30,7 @@ def test_oracle_jets_match_reference(golden, i):
     assert max_rel(lap, golden[f"{t}/jet_lap"]) < 1e-12
 
 
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_oracle_pde_loss_and_gradient(golden, i):
     t, arch, kind, re, act, meta = tape_case(golden, i)
     sq, g, _ = O.pde_loss_grad(golden[f"{t}/params"], arch, act, kind, re, golden[f"{t}/pts"], float(meta[3]))
@@ -38,7 +38,7 @@ def test_oracle_pde_loss_and_gradient(golden, i):
     assert rel_l2(g, golden[f"{t}/grad_pde"]) < 1e-12
 
 
-@pytest.mark.parametrize("i", range(5))
+@pytest.mark.parametrize("i", range(8))
 def test_oracle_mse_loss_and_gradient(golden, i):
     t, arch, kind, re, act, meta = tape_case(golden, i)
     nv = O.REGIMES[kind][1]
