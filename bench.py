@@ -34,6 +34,13 @@ METRIC = "collocation pts/sec (train iters/s) at 1/2/4/8 B200; strong-scaling ef
 UNIT = "colloc_pts/s"
 N_PDE = 500_000
 ARCH = dict(hidden_layers=4, width=64, activation="tanh")
+# --config: the headline strong-scaling config (C) and the other BASELINE.json configs
+CONFIGS = {
+    "C": dict(kind="2d", arch=dict(hidden_layers=4, width=64, activation="tanh"), n_pde=500_000),
+    "D150": dict(kind="2d", arch=dict(hidden_layers=6, width=150, activation="sin"), n_pde=500_000),
+    "D256": dict(kind="2d", arch=dict(hidden_layers=8, width=256, activation="tanh"), n_pde=500_000),
+    "E": dict(kind="3d", arch=dict(hidden_layers=8, width=200, activation="sin"), n_pde=600_000),
+}
 
 
 def flops_per_point(S=6, L=4, W=64, d_in=3, n_out=3):
@@ -138,7 +145,14 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    pb = cylinder2d_problem(n_procs=world, n_pde=args.n_pde, **ARCH)
+    cfgd = CONFIGS[args.config]
+    arch = cfgd["arch"]
+    if cfgd["kind"] == "2d":
+        pb = cylinder2d_problem(n_procs=world, n_pde=args.n_pde, **arch)
+    else:
+        from paper_2602_15883_b200.config import cylinder3d_problem
+
+        pb = cylinder3d_problem(n_procs=world, n_pde=args.n_pde, **arch)
     total_epochs = args.warmup + args.steps + args.e2e_steps + 2
     tc = TrainConfig(epochs=total_epochs, batch_size=25000, learning_rate=1e-3, weights=pb.weights,
                      anchor=pb.anchor, lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0)
@@ -222,15 +236,17 @@ def run_ours(args):
         t_e2e = float(tt.item())
 
     # ---- dominant kernel: the fused PDE jet-MLP fwd+bwd, timed alone ----
-    pde = _time_epoch_kernel(torch, X, worker)
+    pde = _time_epoch_kernel(torch, X, worker) if not worker.objective.wide else _time_wide_pde(torch, X, worker)
     peak = measure_fp32_peak(torch, X) if rank == 0 else None
     if dist is not None:
         dist.barrier()
 
     if rank == 0:
         n_loc = obj.n_colloc
-        fpp = flops_per_point()
-        flops_launch = fpp * n_loc + flops_per_value_point() * pde["n_mse"]
+        rg = pb.domain.regime
+        L, W = arch["hidden_layers"], arch["width"]
+        fpp = flops_per_point(S=1 + rg.n_inputs + rg.n_space, L=L, W=W, d_in=rg.n_inputs, n_out=rg.n_outputs)
+        flops_launch = fpp * n_loc + flops_per_value_point(L, W, rg.n_inputs, rg.n_outputs) * pde["n_mse"]
         achieved = flops_launch / pde["ms"] * 1e-9  # TFLOP/s
         clk = clocks.summary()
         line = {
@@ -248,9 +264,11 @@ def run_ours(args):
             "dtype": "f32" if args.dtype == "float32" else "f64",
             "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
             "config": {
-                "workload": f"2D cylinder-wake strong-scaling, P={world} "
+                "workload": f"{'2D' if cfgd['kind'] == '2d' else '3D'} cylinder-wake strong-scaling, P={world} "
                             f"(decomposition_for_procs), N_pde={args.n_pde}, N_obs={pb.budget.n_obs}, "
-                            f"N_ghost/interface={pb.budget.n_ghost_per_interface}, [3,64x4,3] tanh",
+                            f"N_ghost/interface={pb.budget.n_ghost_per_interface}, "
+                            f"{pb.expert_config.arch[0]},{W}x{L},{pb.expert_config.arch[-1]} {arch['activation']}",
+                "config_id": args.config,
                 "decomposition": [list(pb.subdomains[0].spatial_counts), pb.subdomains[0].time_splits],
                 "colloc_per_rank": n_loc,
                 "l2": "flushed (256 MB write) between timed epochs, outside the events",
@@ -261,7 +279,8 @@ def run_ours(args):
             "launches_per_step": lp,
             "roofline": {
                 "bound": "compute", "pipe": "fp32-simt (FFMA)",
-                "kernel": "jetmlp_epoch_kernel<float,tanh,unsteady2d,64> (fr_epoch_fwd_bwd: PDE + obs/ghost heads)",
+                "kernel": ("jetmlp_epoch_kernel<float,tanh,unsteady2d,64> (fr_epoch_fwd_bwd: PDE + obs/ghost heads)"
+                           if not obj.wide else "layer-wise wide kernels (fr_pde_fwd_bwd, PDE set only)"),
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
                 "peak_source": "measured FP32 FFMA probe (fr_bench_ffma) on this GPU",
@@ -316,6 +335,30 @@ def _time_epoch_kernel(torch, X, worker, reps=10):
     return {"ms": float(np.median(ms)), "n": obj.n_colloc, "n_mse": n_mse}
 
 
+def _time_wide_pde(torch, X, worker, reps=5):
+    """Wide experts: time the PDE set's layer-wise launch sequence alone."""
+    obj = worker.objective
+    sg, mode, kind, n, grow, lrow = [t for t in obj.wide_launches if t[1] == X.MODE_PDE][0]
+    npad = worker.plan.info.np_pad
+
+    def launch():
+        X.call("fr_pde_fwd_bwd", worker.plan.h, X.ptr(worker.kp), X.ptr(obj.col_pts), n,
+               obj.weights.pde / obj.n_colloc, obj.gpart.data_ptr() + 8 * grow * npad,
+               obj.lpart.data_ptr() + 16 * lrow, X.ptr(obj.scratch), X.stream_ptr())
+
+    launch()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        launch()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    return {"ms": float(np.median(ms)), "n": n, "n_mse": 0}
+
+
 def flops_per_value_point(L=4, W=64, d_in=3, n_out=3):
     """Value-stream MSE head fwd+bwd per point (obs / ghost sets)."""
     return 6 * (L - 1) * W * W + 6 * d_in * W + 6 * W * n_out + 10 * L * W
@@ -344,11 +387,18 @@ def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
 
     kind = _reference_module()
     cores = os.cpu_count()
-    from paper_2602_15883_b200.config import cylinder2d_problem
+    from paper_2602_15883_b200.config import cylinder2d_problem, cylinder3d_problem
 
-    pb = cylinder2d_problem(n_procs=1, n_pde=args.n_pde, **ARCH)
+    cfgd = CONFIGS[getattr(args, "config", "C")]
+    arch = cfgd["arch"]
+    make = cylinder2d_problem if cfgd["kind"] == "2d" else cylinder3d_problem
+    pb = make(n_procs=1, n_pde=args.n_pde, **arch)
     ds = pb.datasets[0]
+    if cfgd["kind"] == "3d" or arch["width"] > 64:
+        n_sample = 2_000  # wide nets: keep the CPU sample within the time budget
     sample = ds.colloc_points[:n_sample]
+    rg = pb.domain.regime
+    w = pb.weights
     t_epochs = []
     with threadpool_limits(limits=cores):
         if kind == "reference":
@@ -357,10 +407,10 @@ def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
             from flowrec.physics import FlowRegime, LossWeights
             from flowrec.runtime import AdamState, LocalObjective, adam_step
 
-            regime = FlowRegime("unsteady2d", 100.0)
-            cfg = ExpertConfig.for_regime(regime, 4, 64, "tanh")
-            w = LossWeights(10.0, 5.0, 1.0, 1.0, 1.0)
-            obj = LocalObjective(cfg, regime, RankDatasets(ds.obs_points, ds.obs_velocity, sample, ()), w, 25000)
+            regime = FlowRegime(rg.kind, rg.reynolds)
+            cfg = ExpertConfig.for_regime(regime, arch["hidden_layers"], arch["width"], arch["activation"])
+            lw = LossWeights(w.obs, w.pde, w.ghost_u, w.ghost_p_space, w.ghost_p_time, velocity=w.velocity)
+            obj = LocalObjective(cfg, regime, RankDatasets(ds.obs_points, ds.obs_velocity, sample, ()), lw, 25000)
             params = init_params(cfg, 0)
             st = AdamState.zeros(cfg.n_params)
             rng = np.random.default_rng(0)
@@ -377,12 +427,14 @@ def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
             flat = init_params(pb.expert_config, 0).flat.copy()
             m, v = np.zeros_like(flat), np.zeros_like(flat)
             data = dict(obs_pts=ds.obs_points, obs_vel=ds.obs_velocity, colloc=sample, ghosts=[])
-            wd = dict(obs=10.0, pde=5.0, ghost_u=1.0, ghost_p_space=1.0, ghost_p_time=1.0, velocity=None)
+            wd = dict(obs=w.obs, pde=w.pde, ghost_u=w.ghost_u, ghost_p_space=w.ghost_p_space,
+                      ghost_p_time=w.ghost_p_time, velocity=w.velocity)
             t_end = time.perf_counter() + budget_s
             step = 0
             while time.perf_counter() < t_end or not t_epochs:
                 t0 = time.perf_counter()
-                _, g, _ = O.local_epoch(flat, pb.expert_config.arch, "tanh", "unsteady2d", 100.0, data, wd)
+                _, g, _ = O.local_epoch(flat, pb.expert_config.arch, arch["activation"], rg.kind, rg.reynolds,
+                                        data, wd)
                 step, _ = O.adam_update(flat, g, m, v, step, 1e-3)
                 t_epochs.append(time.perf_counter() - t0)
     t = float(np.median(t_epochs))
@@ -409,8 +461,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": args.n_pde / v * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
             "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
-            "config": {"workload": f"2D cylinder-wake strong-scaling, P=1 epoch sample of N_pde={args.n_pde}, "
-                                   "[3,64x4,3] tanh, reference CPU implementation"},
+            "config": {"workload": f"cylinder-wake strong-scaling config {args.config}, P=1 epoch sample of "
+                                   f"N_pde={args.n_pde}, reference CPU implementation", "config_id": args.config},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -423,11 +475,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
-    ap.add_argument("--n-pde", type=int, default=N_PDE)
+    ap.add_argument("--n-pde", type=int, default=None)
+    ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.n_pde is None:
+        args.n_pde = CONFIGS[args.config]["n_pde"]
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up epochs", file=sys.stderr)
     if args.impl == "reference":

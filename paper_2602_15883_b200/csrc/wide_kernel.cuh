@@ -63,7 +63,13 @@ struct WideCfg {
   __host__ __device__ static size_t gemm_smem() {
     return sizeof(T) * size_t(2 * (KC / 4) * RS4 + 2 * KC * UB);
   }
-  __host__ __device__ static size_t dw_smem() { return sizeof(T) * size_t(2 * 16 * RS4); }
+  // dW staging: a tile's rows in NRC chunks so H + Zbar (16 quads each) fit
+  static constexpr int NRC = (sizeof(T) * 2 * 16 * RS4 > 200 * 1024) ? 2 : 1;
+  static constexpr int RCH = ROWS / NRC;
+  static constexpr int RS4C = sizeof(T) == 4 ? 4 * RCH + ((4 - (4 * RCH) % 32) + 32) % 32
+                                             : 4 * RCH + ((2 - (4 * RCH) % 16) + 16) % 16;
+  static_assert(ROWS % (NRC * DW_SPLIT) == 0, "row chunks must split evenly");
+  __host__ __device__ static size_t dw_smem() { return sizeof(T) * size_t(2 * 16 * RS4C); }
 };
 
 struct WInfo {
@@ -562,10 +568,12 @@ __global__ void __launch_bounds__(256) wide_dx_kernel(WArgs a, int l) {
 template <typename T, int ACT, int MODE, int REG>
 __global__ void __launch_bounds__(256) wide_dw_kernel(WArgs a, int l) {
   using C = WideCfg<T, ACT, MODE, REG>;
-  constexpr int RS4 = C::RS4, ROWS = C::ROWS, SPLIT = C::DW_SPLIT, RROWS = ROWS / SPLIT, FLUSH = 8;
+  constexpr int ROWS = C::ROWS, SPLIT = C::DW_SPLIT, FLUSH = 8;
+  constexpr int RS4C = C::RS4C, RCH = C::RCH, NRC = C::NRC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Hs = reinterpret_cast<T*>(smem_raw);  // 16 quads
-  T* Zs = Hs + 16 * RS4;
+  T* Hs = reinterpret_cast<T*>(smem_raw);  // 16 quads x RCH rows
+  T* Zs = Hs + 16 * RS4C;
+  static_assert(2 * 16 * RS4C >= (SPLIT - 1) * 4096, "combine scratch must fit in the staging buffers");
   const int kb = blockIdx.x, ubk = blockIdx.y, ks = blockIdx.z;
   const int tid = threadIdx.x, ut = tid % 8, kt = (tid / 8) % 8, rs = tid / 64;
   const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
@@ -621,39 +629,44 @@ __global__ void __launch_bounds__(256) wide_dw_kernel(WArgs a, int l) {
   for (long long t = ks; t < a.ntiles; t += gridDim.z) {
     const T* hsrc = static_cast<const T*>(a.act) + act_off<C>(a, l - 1, t, kb * 16);
     const T* zsrc = static_cast<const T*>(a.adj) + act_off<C>(a, l, t, ubk * 16);
-    constexpr int QCH = ROWS * 4 * int(sizeof(T)) / 16;
-    for (int i = tid; i < 16 * QCH; i += 256) {
-      const int qq = i / QCH, o = i % QCH;
-      cp_async16(reinterpret_cast<char*>(Hs + qq * RS4) + 16 * o,
-                 reinterpret_cast<const char*>(hsrc + size_t(qq) * (ROWS * 4)) + 16 * o);
-      cp_async16(reinterpret_cast<char*>(Zs + qq * RS4) + 16 * o,
-                 reinterpret_cast<const char*>(zsrc + size_t(qq) * (ROWS * 4)) + 16 * o);
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    const T* x0 = Hs + kt * RS4 + 4 * (rs * RROWS);
-    const T* x1 = Hs + (kt + 8) * RS4 + 4 * (rs * RROWS);
-    const T* z0 = Zs + ut * RS4 + 4 * (rs * RROWS);
-    const T* z1 = Zs + (ut + 8) * RS4 + 4 * (rs * RROWS);
+#pragma unroll 1
+    for (int ch = 0; ch < NRC; ++ch) {
+      constexpr int QCH = RCH * 4 * int(sizeof(T)) / 16;  // 16-byte chunks of one quad's row chunk
+      for (int i = tid; i < 16 * QCH; i += 256) {
+        const int qq = i / QCH, o = i % QCH;
+        const size_t go = size_t(qq) * (ROWS * 4) + size_t(ch) * RCH * 4;
+        cp_async16(reinterpret_cast<char*>(Hs + qq * RS4C) + 16 * o, reinterpret_cast<const char*>(hsrc + go) + 16 * o);
+        cp_async16(reinterpret_cast<char*>(Zs + qq * RS4C) + 16 * o, reinterpret_cast<const char*>(zsrc + go) + 16 * o);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+      // rows rs, rs + SPLIT, ... of this chunk (strided: balanced across chunks)
+      const T* x0 = Hs + kt * RS4C;
+      const T* x1 = Hs + (kt + 8) * RS4C;
+      const T* z0 = Zs + ut * RS4C;
+      const T* z1 = Zs + (ut + 8) * RS4C;
 #pragma unroll 2
-    for (int r = 0; r < RROWS; ++r) {
-      T h[8], z[8];
-      vload(*reinterpret_cast<T(*)[4]>(h), x0 + 4 * r);
-      vload(*reinterpret_cast<T(*)[4]>(h + 4), x1 + 4 * r);
-      vload(*reinterpret_cast<T(*)[4]>(z), z0 + 4 * r);
-      vload(*reinterpret_cast<T(*)[4]>(z + 4), z1 + 4 * r);
+      for (int r = rs; r < RCH; r += SPLIT) {
+        T h[8], z[8];
+        vload(*reinterpret_cast<T(*)[4]>(h), x0 + 4 * r);
+        vload(*reinterpret_cast<T(*)[4]>(h + 4), x1 + 4 * r);
+        vload(*reinterpret_cast<T(*)[4]>(z), z0 + 4 * r);
+        vload(*reinterpret_cast<T(*)[4]>(z + 4), z1 + 4 * r);
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
+        for (int x = 0; x < 8; ++x)
 #pragma unroll
-        for (int y = 0; y < 8; ++y) acc[x][y] = fma(h[x], z[y], acc[x][y]);
+          for (int y = 0; y < 8; ++y) acc[x][y] = fma(h[x], z[y], acc[x][y]);
+      }
+      if (kb == 0 && tid < 64) {
+        const T* zq = Zs + (tid / 4) * RS4C + (tid % 4);
+        for (int pt = 0; pt < C::PPT; ++pt) {
+          const int row = (C::JET ? pt * C::S : pt) - ch * RCH;  // value rows in this chunk
+          if (row >= 0 && row < RCH) db += zq[4 * row];
+        }
+      }
+      __syncthreads();
     }
-    if (kb == 0 && tid < 64) {
-      const int u = tid;  // value rows: every S-th row (jet) or every row (value modes)
-      const T* zq = Zs + (u / 4) * RS4 + (u % 4);
-      for (int pt = 0; pt < C::PPT; ++pt) db += zq[4 * (C::JET ? pt * C::S : pt)];
-    }
-    __syncthreads();
     if (++since == FLUSH) {
       flush();
       since = 0;
