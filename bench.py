@@ -300,14 +300,16 @@ def run_ours(args):
 
 
 def _launches_per_epoch(trainer, X):
+    """Kernels this library enqueues for one epoch, counted by the library
+    itself while one epoch's work is being captured (capture does not run it)."""
     import torch
 
-    before = X.launch_count
+    before = X.kernel_launches()
     g = torch.cuda.CUDAGraph()
     torch.cuda.synchronize()
     with torch.cuda.graph(g):
         trainer._enqueue(True)
-    n = X.launch_count - before
+    n = X.kernel_launches() - before
     del g
     return n
 

@@ -175,6 +175,9 @@ int fr_jet_act_backward(int kind, const double* z, const double* s, const double
  * threads, each running `iters` x 64 independent FMA chains of 8; out[grid*256] */
 int fr_bench_ffma(int grid, int iters, int unused, float* out, fr_stream_t stream);
 
+/* running count of kernels enqueued by this library (host-side counter) */
+long long fr_kernel_launches(void);
+
 const char* fr_last_error(void);
 const char* fr_version(void);
 

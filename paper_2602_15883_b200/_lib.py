@@ -92,7 +92,7 @@ _SIGS = {
     "fr_jet_act_backward": [C.c_int, _P, _P, _P, _P, _P, C.c_longlong, C.c_int, C.c_int, C.c_int, _P],
     "fr_bench_ffma": [C.c_int, C.c_int, C.c_int, _P, _P],
 }
-EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version")
+EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version", "fr_kernel_launches")
 
 _lib = None
 
@@ -116,6 +116,8 @@ def lib():
     L.fr_last_error.argtypes = []
     L.fr_version.restype = C.c_char_p
     L.fr_version.argtypes = []
+    L.fr_kernel_launches.restype = C.c_longlong
+    L.fr_kernel_launches.argtypes = []
     _lib = L
     return L
 
@@ -140,6 +142,11 @@ def call(name, *args):
         msg = L.fr_last_error().decode(errors="replace")
         raise FlowrecError(f"{name}: {msg}")
     return rc
+
+
+def kernel_launches():
+    """Kernels enqueued by the library so far (for launch accounting)."""
+    return int(lib().fr_kernel_launches())
 
 
 def version():

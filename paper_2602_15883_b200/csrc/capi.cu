@@ -28,7 +28,12 @@ int wide_entry_f64(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 }  // namespace fr
 
+namespace fr {
+long long g_kernel_launches = 0;
+}
 using namespace fr;
+
+extern "C" long long fr_kernel_launches(void) { return g_kernel_launches; }
 
 static thread_local std::string g_err;
 
@@ -332,6 +337,7 @@ extern "C" int fr_prepare_params(const fr_plan* p, const double* flat, void* kpa
     prepare_kernel<float><<<blocks, 256, 0, stream>>>(flat, p->d_inv, static_cast<float*>(kparams), n);
   else
     prepare_kernel<double><<<blocks, 256, 0, stream>>>(flat, p->d_inv, static_cast<double*>(kparams), n);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_prepare_params");
   return 0;
 }
@@ -524,6 +530,7 @@ extern "C" int fr_reduce_grad(const fr_plan* p, const double* gpart, int rows, d
   if (rows <= 0 && accumulate && !norm_parts) return 0;
   reduce_grad_kernel<<<(n + RG_P - 1) / RG_P, RG_P * RG_R, 0, stream>>>(gpart, rows > 0 ? rows : 0, p->info.np_pad,
                                                                         p->d_map, n, grad, accumulate, norm_parts);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_reduce_grad");
   return 0;
 }
@@ -558,6 +565,7 @@ extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int
   }
   if (total > 0 && !lpart) return fail("fr_reduce_loss: NULL lpart");
   reduce_loss_kernel<<<1, 32, 0, stream>>>(lpart, seg, sums);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_reduce_loss");
   return 0;
 }
@@ -705,6 +713,7 @@ extern "C" int fr_adam_step(const fr_plan* p, const fr_adam_args* args, fr_strea
     adam_kernel<float><<<blocks, ADAM_NT, 0, stream>>>(*args, n, map, mapT);
   else
     adam_kernel<double><<<blocks, ADAM_NT, 0, stream>>>(*args, n, map, mapT);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_adam_step");
   return 0;
 }
@@ -733,6 +742,7 @@ extern "C" int fr_pack_ghost(const fr_plan* p, const void* y, const void* y_anch
     pack_ghost_kernel<double><<<blocks, 256, 0, stream>>>(static_cast<const double*>(y), static_cast<const double*>(y_anchor),
                                                           n, p->info.n_out, p->info.n_vel, static_cast<double*>(out_u),
                                                           static_cast<double*>(out_p));
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_pack_ghost");
   return 0;
 }
@@ -805,6 +815,7 @@ extern "C" int fr_jet_act_forward(int kind, const double* z, double* s, const do
   if (total == 0) return 0;
   const int blocks = int((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   act_fwd_kernel<<<blocks, 256, 0, stream>>>(kind, z, s, aux, d1, d2, batch, n_inputs, width);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_jet_act_forward");
   return 0;
 }
@@ -819,6 +830,7 @@ extern "C" int fr_jet_act_backward(int kind, const double* z, const double* s, c
   if (total == 0) return 0;
   const int blocks = int((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   act_bwd_kernel<<<blocks, 256, 0, stream>>>(kind, z, s, aux, sbar, zbar, batch, n_inputs, width, accumulate);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_jet_act_backward");
   return 0;
 }
@@ -847,6 +859,7 @@ __global__ void __launch_bounds__(256) ffma_kernel(int iters, float* out) {
 extern "C" int fr_bench_ffma(int grid, int iters, int, float* out, fr_stream_t stream) {
   if (grid < 1 || iters < 1 || !out) return fail("fr_bench_ffma: bad arguments");
   ffma_kernel<<<grid, 256, 0, stream>>>(iters, out);
+  ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_bench_ffma");
   return 0;
 }

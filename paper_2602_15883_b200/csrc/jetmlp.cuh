@@ -17,18 +17,24 @@
 // the pre-activation derivative streams that the backward sweep re-reads.
 //
 // Layouts (all in shared memory):
-//   activations / adjoints: "k-pair" layout  A[(k>>1)*RS2 + row*2 + (k&1)],
-//       row = point*S + stream (jet modes) or row = point (value modes);
+//   activations / adjoints: k-quad layout A[(k>>2)*RS4 + row*4 + (k&3)] with
+//       RS4 padded to 4 banks mod 32, row = point*S + stream (jet modes) or
+//       row = point (value modes) -- every LDS.128 / STS.128 conflict-free;
 //   weight slots: row-major [W][W] copies of W_l (forward) or W_l^T (dX),
-//       double-buffered with cp.async;
-// Gradient partials are accumulated per CTA in FP64 (fixed ownership, no
-// atomics) and reduced across CTAs in a fixed order by fr_reduce_rows, so a
-// rerun is bit-identical (the reference's determinism contract, tape.py:1-6).
+//       double-buffered with cp.async.
+// Gradient partials are accumulated per CTA in FP64 with red.add, each address
+// of a CTA's row written by exactly one thread, and reduced across CTAs in a
+// fixed order by fr_reduce_grad, so a rerun is bit-identical (the reference's
+// determinism contract, tape.py:1-6).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace fr {
+
+// running count of kernels this library has enqueued (host side; the bench's
+// gpu_launches claim is a difference of this counter around one epoch)
+extern long long g_kernel_launches;
 
 enum { ACT_TANH = 0, ACT_SIN = 1 };
 enum { REG_STEADY2D = 0, REG_UNSTEADY2D = 1, REG_UNSTEADY3D = 2 };

@@ -54,6 +54,7 @@ int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
     smem_set = smem;
   }
   k<<<grid, C::NT, smem, st>>>(*a);
+  ++g_kernel_launches;
   return int(cudaGetLastError());
 }
 
@@ -79,6 +80,7 @@ int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L)
     smem_set = smem;
   }
   k<<<grid, CP::NT, smem, st>>>(*e);
+  ++g_kernel_launches;
   return int(cudaGetLastError());
 }
 

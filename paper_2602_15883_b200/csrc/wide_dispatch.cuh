@@ -35,7 +35,9 @@ int run_wide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
     for (int l = a.L - 1; l >= 1; --l) wide_dw_kernel<T, ACT, MODE, REG><<<gw, C::DW_NT, C::dw_smem(), st>>>(a, l);
     wide_dwL_kernel<T, ACT, MODE, REG><<<ks, 256, 0, st>>>(a);
     wide_dw0_kernel<T, ACT, MODE, REG><<<dim3(ks, (a.WP + 255) / 256), 256, 0, st>>>(a);
+    g_kernel_launches += 2 * (a.L - 1) + 2;
   }
+  g_kernel_launches += a.L + 1;
   return int(cudaGetLastError());
 }
 
