@@ -139,6 +139,8 @@ def run_ours(args):
     world, rank, local = _dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.local_ranks and world > 1:
+        raise SystemExit("--local-ranks runs every subdomain on one GPU (N=1 only)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -147,12 +149,13 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfgd = CONFIGS[args.config]
     arch = cfgd["arch"]
+    n_sub = args.local_ranks or world
     if cfgd["kind"] == "2d":
-        pb = cylinder2d_problem(n_procs=world, n_pde=args.n_pde, **arch)
+        pb = cylinder2d_problem(n_procs=n_sub, n_pde=args.n_pde, **arch)
     else:
         from paper_2602_15883_b200.config import cylinder3d_problem
 
-        pb = cylinder3d_problem(n_procs=world, n_pde=args.n_pde, **arch)
+        pb = cylinder3d_problem(n_procs=n_sub, n_pde=args.n_pde, **arch)
     total_epochs = args.warmup + args.steps + args.e2e_steps + 2
     tc = TrainConfig(epochs=total_epochs, batch_size=25000, learning_rate=1e-3, weights=pb.weights,
                      anchor=pb.anchor, lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0)
@@ -212,7 +215,8 @@ def run_ours(args):
 
     # ---- e2e: host pinned inputs copied in + loss row copied out every step ----
     obj = worker.objective
-    dev_bufs = [obj.col_pts, obj.obs_pts, obj.obs_vel] + [g["pts"] for g in obj.ghost.values()]
+    objs = [w.objective for w in trainer.workers.values()] if world == 1 else [obj]
+    dev_bufs = [b for o in objs for b in [o.col_pts, o.obs_pts, o.obs_vel] + [g["pts"] for g in o.ghost.values()]]
     host_bufs = [b.cpu().pin_memory() for b in dev_bufs]
     h2d = sum(b.numel() * b.element_size() for b in host_bufs)
     row_host = torch.empty(7, dtype=torch.float64).pin_memory()
@@ -264,11 +268,12 @@ def run_ours(args):
             "dtype": "f32" if args.dtype == "float32" else "f64",
             "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
             "config": {
-                "workload": f"{'2D' if cfgd['kind'] == '2d' else '3D'} cylinder-wake strong-scaling, P={world} "
+                "workload": f"{'2D' if cfgd['kind'] == '2d' else '3D'} cylinder-wake strong-scaling, P={n_sub} "
                             f"(decomposition_for_procs), N_pde={args.n_pde}, N_obs={pb.budget.n_obs}, "
                             f"N_ghost/interface={pb.budget.n_ghost_per_interface}, "
                             f"{pb.expert_config.arch[0]},{W}x{L},{pb.expert_config.arch[-1]} {arch['activation']}",
                 "config_id": args.config,
+                "subdomains_on_this_gpu": len(pb.subdomains) if world == 1 else 1,
                 "decomposition": [list(pb.subdomains[0].spatial_counts), pb.subdomains[0].time_splits],
                 "colloc_per_rank": n_loc,
                 "l2": "flushed (256 MB write) between timed epochs, outside the events",
@@ -479,6 +484,8 @@ def main():
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--n-pde", type=int, default=None)
     ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
+    ap.add_argument("--local-ranks", type=int, default=0,
+                    help="run all P subdomains of decomposition_for_procs(P) on this one GPU (serial backend)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

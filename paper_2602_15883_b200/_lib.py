@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libflowrec_b200.so")
+LIB_PATH = os.environ.get("FLOWREC_B200_LIB") or os.path.join(HERE, "_lib", "libflowrec_b200.so")
 
 ACT_TANH, ACT_SIN = 0, 1
 STEADY2D, UNSTEADY2D, UNSTEADY3D = 0, 1, 2

@@ -47,36 +47,41 @@ def needs_build():
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def _compile(src):
-    obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, defines=(), out_dir=OUT_DIR):
+    obj = os.path.join(out_dir, os.path.splitext(src)[0] + ".o")
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force=False, jobs=None, verbose=False):
-    """Compile every CUDA translation unit for sm_100a and link the shared library."""
-    if not force and not needs_build():
+def build(force=False, jobs=None, verbose=False, defines=(), lib=None):
+    """Compile every CUDA translation unit for sm_100a and link the shared library.
+
+    `defines` / `lib` produce instrumented side builds (e.g. FR_PHASE_TIMERS into
+    another path, selected at run time with FLOWREC_B200_LIB)."""
+    lib = lib or LIB
+    if not force and lib == LIB and not needs_build():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    out_dir = os.path.dirname(os.path.abspath(lib))
+    os.makedirs(out_dir, exist_ok=True)
     jobs = jobs or min(len(SOURCES), os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
-        results = list(ex.map(_compile, SOURCES))
+        results = list(ex.map(lambda src: _compile(src, defines, out_dir), SOURCES))
     for obj, log in results:
         if verbose and log.strip():
             print(log, file=sys.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            *[o for o, _ in results], "-o", tmp, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o, _ in results:
         os.remove(o)
-    return LIB
+    return lib
 
 
 def main():
@@ -84,8 +89,10 @@ def main():
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", "--jobs", type=int, default=None)
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("-D", "--define", action="append", default=[], help="extra -D for an instrumented side build")
+    ap.add_argument("--lib", default=None, help="output path (side builds)")
     a = ap.parse_args()
-    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose))
+    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose, defines=a.define, lib=a.lib))
 
 
 if __name__ == "__main__":

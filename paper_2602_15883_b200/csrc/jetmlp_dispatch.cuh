@@ -117,10 +117,24 @@ int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cuda
     return dispatch_mode_t<MODE_##M, T>(act, reg, w, a, grid, st, info, L);                           \
   }                                                                                                   \
   }
+#ifdef FR_PHASE_TIMERS
+#define FR_PHASE_READER(TAG)                                                          \
+  extern "C" int fr_debug_phase_cycles_##TAG(unsigned long long* out, int reset) {    \
+    cudaMemcpyFromSymbol(out, fr::g_phase_cycles, sizeof(unsigned long long) * 16);   \
+    if (reset) {                                                                      \
+      unsigned long long z[16] = {0};                                                 \
+      cudaMemcpyToSymbol(fr::g_phase_cycles, z, sizeof(z));                           \
+    }                                                                                 \
+    return 0;                                                                         \
+  }
+#else
+#define FR_PHASE_READER(TAG)
+#endif
 #define FR_DEFINE_EPOCH_ENTRY(T, TAG)                                                                  \
   namespace fr {                                                                                      \
   int epoch_entry_##TAG(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st,        \
                         KInfo* info, int L) {                                                         \
     return dispatch_epoch_t<T>(act, reg, w, e, grid, st, info, L);                                    \
   }                                                                                                   \
-  }
+  }                                                                                                   \
+  FR_PHASE_READER(TAG)

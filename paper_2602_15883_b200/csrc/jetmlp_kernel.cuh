@@ -4,6 +4,23 @@
 
 namespace fr {
 
+// optional per-phase cycle counters (instrumented builds only: -DFR_PHASE_TIMERS)
+#ifdef FR_PHASE_TIMERS
+__device__ unsigned long long g_phase_cycles[16];
+#define FR_MARK(id)                         \
+  do {                                      \
+    if (threadIdx.x == 0) {                 \
+      const long long t_ = clock64();       \
+      ph_acc[id] += t_ - ph_last;           \
+      ph_last = t_;                         \
+    }                                       \
+  } while (0)
+#else
+#define FR_MARK(id) \
+  do {              \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // scalar math (accurate libm versions: first-layer arguments reach |z|~17 on
 // the cylinder box, so tanh.approx / __sinf are not acceptable)
@@ -117,7 +134,11 @@ struct JetCfg {
   static constexpr int PP = JET ? 1 : RPT;      // points per thread
   static constexpr int SIN = (ACT == ACT_SIN) ? 1 : 0;
   static constexpr int NST0 = 1 + SIN;                       // layer-0 stash / (point,unit)
-  static constexpr int NSTH = JET ? (1 + SIN + NG + NL) : NST0;  // hidden-layer stash
+  // hidden-layer stash per (point, unit), jet modes: the layer's S output
+  // streams (rebuild the next layer's input without recomputation) and S
+  // adjoint factors {d1, d2*z_g[i], d3*z_g[j]^2 + d2*z_l[j]} so the activation
+  // adjoint is a handful of FMAs
+  static constexpr int NSTH = JET ? 2 * S : NST0;
   // k-quad layout: element (row, k) at (k>>2)*RS4 + row*4 + (k&3).  RS4 is
   // padded so that consecutive quads start 4 banks apart: the 8 lanes of a
   // quarter-warp touching 8 consecutive quads then cover all 32 banks.
@@ -131,7 +152,7 @@ struct JetCfg {
   // largest split with one thread per (tile, range), rows divisible, and the
   // R-1 partials of the flat combine fitting in the activation buffer
   static constexpr int rsplit_fit(int r) {
-    return (r > 1 && (r * KT * KT > NT || (r - 1) * W * W > XELEMS || ROWS % r != 0)) ? rsplit_fit(r - 1) : r;
+    return (r > 1 && (r * KT * KT > NT || r * W * W > XELEMS || ROWS % r != 0)) ? rsplit_fit(r - 1) : r;
   }
   static constexpr int RSPLIT = rsplit_fit(NT / (KT * KT) > 0 ? NT / (KT * KT) : 1);
   static_assert(W % 8 == 0, "width must be a multiple of 8");
@@ -327,6 +348,10 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   __syncthreads();
 
   const long long ntiles = (n + PPT - 1) / PPT;
+#ifdef FR_PHASE_TIMERS
+  long long ph_acc[16] = {0};
+  long long ph_last = clock64();
+#endif
   for (long long tile = t0; tile < ntiles; tile += tstride) {
     const long long p0 = tile * PPT;
     {
@@ -343,6 +368,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       }
     }
     __syncthreads();
+    FR_MARK(0);
 
     // ---------------- layer 0 (DIN -> W): derivative blocks are constant ----------------
     {
@@ -383,6 +409,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
     }
     __syncthreads();
+    FR_MARK(1);
 
     // ---------------- hidden layers 1..L-1 ----------------
     for (int l = 1; l < L; ++l) {
@@ -391,6 +418,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       T acc[RPT][8];
       gemm_rows<T, W, RPT, RS4>(Xs, Bm, rg, g, acc);
       __syncthreads();
+      FR_MARK(2);
       T outv[RPT][8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -411,12 +439,17 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           }
           if constexpr (BWD) {
             const int q = j * NSTH;
-            stash[st_idx(l, q)] = s;
-            if constexpr (C::SIN) stash[st_idx(l, q + 1)] = c;
+            const T d3 = act_d3<ACT>(s, c, d1, d2);
 #pragma unroll
-            for (int i = 0; i < NG; ++i) stash[st_idx(l, q + 1 + C::SIN + i)] = acc[1 + i][j];
+            for (int st = 0; st < S; ++st) stash[st_idx(l, q + st)] = outv[st][j];
+            stash[st_idx(l, q + S)] = d1;
 #pragma unroll
-            for (int i = 0; i < NL; ++i) stash[st_idx(l, q + 1 + C::SIN + NG + i)] = acc[1 + NG + i][j];
+            for (int i = 0; i < NG; ++i) stash[st_idx(l, q + S + 1 + i)] = d2 * acc[1 + i][j];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+              const T zg = acc[1 + LAP0 + i][j];
+              stash[st_idx(l, q + S + 1 + NG + i)] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
+            }
           }
         } else {
 #pragma unroll
@@ -435,6 +468,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
       cp_async_wait_all();
       __syncthreads();
+      FR_MARK(3);
       ++ws;
     }
 
@@ -457,6 +491,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       for (int c = 0; c < NOUT; ++c) Ys[r * NOUT + c] = vrow ? y[c] + bLs[c] : y[c];
     }
     __syncthreads();
+    FR_MARK(4);
 
     // ---------------- head ----------------
     const long long rem = n - p0;
@@ -558,24 +593,52 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       }
     }
     __syncthreads();
+    FR_MARK(5);
 
     if constexpr (BWD) {
       // ---------------- output layer backward ----------------
-      for (int i = tid; i < W * NOUT; i += NT) {
-        const int k = i / NOUT, c = i % NOUT;
-        T s4[4] = {T(0), T(0), T(0), T(0)};  // four independent chains
-        static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
-#pragma unroll 2
-        for (int r = 0; r < ROWS; r += 4)
+      // dW_L = H_L^T Ybar: thread (k-quad, row split) accumulates 4 k x NOUT over
+      // its rows; the partials meet in Gs (free until dX_L) in a fixed order.
+      {
+        constexpr int KQ = W / 4, RSL = NT / KQ;
+        static_assert(NT % KQ == 0 && RSL * W * NOUT <= C::XELEMS, "output-layer split must fit");
+        const int kq = tid % KQ, rsl = tid / KQ;
+        T acc[4][NOUT];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) s4[q] = fma(Xs[kqi<RS4>(r + q, k)], Ybs[(r + q) * NOUT + c], s4[q]);
-        red_add(gp + pl.off_w(L) + i, double((s4[0] + s4[1]) + (s4[2] + s4[3])));
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int c = 0; c < NOUT; ++c) acc[x][c] = T(0);
+        const T* xp = Xs + kq * RS4;
+#pragma unroll 2
+        for (int r = rsl; r < ROWS; r += RSL) {
+          T hv[4];
+          vload(hv, xp + 4 * r);
+#pragma unroll
+          for (int c = 0; c < NOUT; ++c) {
+            const T yb = Ybs[r * NOUT + c];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) acc[x][c] = fma(hv[x], yb, acc[x][c]);
+          }
+        }
+        T* part = Gs + rsl * (W * NOUT);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int c = 0; c < NOUT; ++c) part[(4 * kq + x) * NOUT + c] = acc[x][c];
+      }
+      __syncthreads();
+      for (int i = tid; i < W * NOUT; i += NT) {
+        constexpr int RSL = NT / (W / 4);
+        T s = Gs[i];
+        for (int q = 1; q < RSL; ++q) s += Gs[q * (W * NOUT) + i];
+        red_add(gp + pl.off_w(L) + i, double(s));
       }
       if (tid < NOUT) {
         T s = T(0);
         for (int pt = 0; pt < PPT; ++pt) s += Ybs[(JET ? pt * S : pt) * NOUT + tid];
         red_add(gp + pl.off_b(L) + tid, double(s));
       }
+      __syncthreads();
       {
         T gv[RPT][8];
 #pragma unroll
@@ -593,6 +656,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         store_block<T, W, RPT, RS4>(Gs, rg, g, gv);
       }
       __syncthreads();
+      FR_MARK(6);
 
       // ---------------- hidden layers L-1..1 ----------------
       for (int l = L - 1; l >= 1; --l) {
@@ -604,30 +668,24 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if constexpr (JET) {
-              const int q = j * NSTH;
-              const T s = stash[st_idx(l, q)];
-              const T c = C::SIN ? stash[st_idx(l, q + 1)] : T(0);
-              T zg[NG], zl[NL > 0 ? NL : 1];
+              // numpy_backend.py:58-89 with the forward-time factors
+              const int q = j * NSTH + S;
+              const T d1 = stash[st_idx(l, q)];
+              T ga[NG], lb[NL > 0 ? NL : 1];
 #pragma unroll
-              for (int i = 0; i < NG; ++i) zg[i] = stash[st_idx(l, q + 1 + C::SIN + i)];
+              for (int i = 0; i < NG; ++i) ga[i] = stash[st_idx(l, q + 1 + i)];
 #pragma unroll
-              for (int i = 0; i < NL; ++i) zl[i] = stash[st_idx(l, q + 1 + C::SIN + NG + i)];
-              T d1, d2;
-              act_d12<ACT>(s, c, d1, d2);
-              const T d3 = act_d3<ACT>(s, c, d1, d2);
+              for (int i = 0; i < NL; ++i) lb[i] = stash[st_idx(l, q + 1 + NG + i)];
               T zv = sb[0][j] * d1;
 #pragma unroll
-              for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * (d2 * zg[i]);
+              for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * ga[i];
 #pragma unroll
-              for (int i = 0; i < NL; ++i) {
-                const T gg = zg[LAP0 + i];
-                zv += sb[1 + NG + i][j] * (d3 * gg * gg + d2 * zl[i]);
-              }
+              for (int i = 0; i < NL; ++i) zv += sb[1 + NG + i][j] * lb[i];
               zb[0][j] = zv;
 #pragma unroll
               for (int i = 0; i < NG; ++i) {
                 T t = sb[1 + i][j] * d1;
-                if (i >= LAP0) t += (T(2) * d2) * zg[i] * sb[1 + NG + (i - LAP0)][j];
+                if (i >= LAP0) t += (T(2) * ga[i]) * sb[1 + NG + (i - LAP0)][j];
                 zb[1 + i][j] = t;
               }
 #pragma unroll
@@ -653,14 +711,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           for (int j = 0; j < 8; ++j) {
             const int u = unit_of<W>(g, j);
             if constexpr (JET) {
-              const int nst = lp == 0 ? NST0 : NSTH;
-              const int q = j * nst;
-              const T s = stash[st_idx(lp, q)];
-              const T c = C::SIN ? stash[st_idx(lp, q + 1)] : T(0);
-              T d1, d2;
-              act_d12<ACT>(s, c, d1, d2);
-              hv[0][j] = s;
               if (lp == 0) {
+                const T s = stash[st_idx(0, j * NST0)];
+                const T c = C::SIN ? stash[st_idx(0, j * NST0 + 1)] : T(0);
+                T d1, d2;
+                act_d12<ACT>(s, c, d1, d2);
+                hv[0][j] = s;
 #pragma unroll
                 for (int i = 0; i < NG; ++i) hv[1 + i][j] = d1 * W0s[i * W + u];
 #pragma unroll
@@ -669,18 +725,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                   hv[1 + NG + i][j] = d2 * zg * zg;
                 }
               } else {
-                T zg[NG];
 #pragma unroll
-                for (int i = 0; i < NG; ++i) {
-                  zg[i] = stash[st_idx(lp, q + 1 + C::SIN + i)];
-                  hv[1 + i][j] = d1 * zg[i];
-                }
-#pragma unroll
-                for (int i = 0; i < NL; ++i) {
-                  const T zl = stash[st_idx(lp, q + 1 + C::SIN + NG + i)];
-                  const T gg = zg[LAP0 + i];
-                  hv[1 + NG + i][j] = d2 * gg * gg + d1 * zl;
-                }
+                for (int st = 0; st < S; ++st) hv[st][j] = stash[st_idx(lp, j * NSTH + st)];
               }
             } else {
 #pragma unroll
@@ -690,6 +736,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           store_block<T, W, RPT, RS4>(Xs, rg, g, hv);
         }
         __syncthreads();
+        FR_MARK(7);
         stage(ws + 1);
 
         // dW_l = H_l^T Zbar_l over all rows of the tile.  Thread tile 8k x 8u
@@ -730,38 +777,28 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             red_add(gp + pl.off_b(l) + tid, double(sb));
           }
           __syncthreads();  // every read of Xs (H_l) is done: reuse it as scratch
-          // combine the RSPLIT row-range partials in a fixed order (rs = 1, 2, ...)
+          FR_MARK(8);
+          // combine the RSPLIT row-range partials: every thread sums a strided
+          // slice of the 64x64 block over rs = 0, 1, ... (fixed order) and
+          // red.adds it once
           auto kidx = [&](int x) { return x < 4 ? 4 * kt + x : 4 * (kt + KT) + (x - 4); };
-          if (active && rs > 0) {
-            T* dst = Xs + (rs - 1) * W * W;
+          if (active) {
+            T* dst = Xs + rs * W * W;
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
               vstore(dst + kidx(x) * W + 4 * ut, *reinterpret_cast<const T(*)[4]>(&acc[x][0]));
               vstore(dst + kidx(x) * W + 4 * (ut + KT), *reinterpret_cast<const T(*)[4]>(&acc[x][4]));
             }
           }
+          FR_MARK(9);
           __syncthreads();
-          if (active && rs == 0) {
+          {
             double* dst = gp + pl.off_w(l);
+            for (int e = tid; e < W * W; e += NT) {
+              T sum = Xs[e];
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-              const int k = kidx(x);
-              for (int q = 1; q < RSPLIT; ++q) {
-                const T* src = Xs + (q - 1) * W * W + k * W;
-                T a4[4], b4[4];
-                vload(a4, src + 4 * ut);
-                vload(b4, src + 4 * (ut + KT));
-#pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                  acc[x][y] += a4[y];
-                  acc[x][4 + y] += b4[y];
-                }
-              }
-#pragma unroll
-              for (int y = 0; y < 4; ++y) {
-                red_add(dst + k * W + 4 * ut + y, double(acc[x][y]));
-                red_add(dst + k * W + 4 * (ut + KT) + y, double(acc[x][4 + y]));
-              }
+              for (int q = 1; q < RSPLIT; ++q) sum += Xs[q * W * W + e];
+              red_add(dst + e, double(sum));
             }
           }
         }
@@ -771,10 +808,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           T acc[RPT][8];
           gemm_rows<T, W, RPT, RS4>(Gs, Bm, rg, g, acc);
           __syncthreads();
+          FR_MARK(10);
           store_block<T, W, RPT, RS4>(Gs, rg, g, acc);
         }
         cp_async_wait_all();
         __syncthreads();
+        FR_MARK(11);
         ++ws;
       }
 
@@ -826,6 +865,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         store_block<T, W, RPT, RS4>(Gs, rg, g, zb);
       }
       __syncthreads();
+      FR_MARK(12);
       // dW0 = X^T Zbar over the stacked input (value rows hold the points, the
       // derivative block j is the unit vector e_j, tape.py:426-436); db0.
       for (int i = tid; i < (DIN + 1) * W; i += NT) {
@@ -844,6 +884,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         }
       }
       __syncthreads();
+      FR_MARK(13);
     }
   }
 
@@ -862,6 +903,10 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       lpart_row[1] = s1;
     }
   }
+#ifdef FR_PHASE_TIMERS
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 16; ++i) atomicAdd(&g_phase_cycles[i], (unsigned long long)ph_acc[i]);
+#endif
   __syncthreads();  // shared memory is reused by the caller's next dataset
 }
 
