@@ -175,6 +175,10 @@ int fr_jet_act_backward(int kind, const double* z, const double* s, const double
  * threads, each running `iters` x 64 independent FMA chains of 8; out[grid*256] */
 int fr_bench_ffma(int grid, int iters, int unused, float* out, fr_stream_t stream);
 
+/* tcgen05 probe: C[128][N] = A[128][K] * B[N][K]^T in TF32 on the tensor core,
+ * accumulator in TMEM (16 <= N <= 256, N % 16 == 0, K % 8 == 0, K <= 64) */
+int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, fr_stream_t stream);
+
 /* running count of kernels enqueued by this library (host-side counter) */
 long long fr_kernel_launches(void);
 

@@ -91,6 +91,7 @@ _SIGS = {
     "fr_jet_act_forward": [C.c_int, _P, _P, _P, _P, _P, C.c_longlong, C.c_int, C.c_int, _P],
     "fr_jet_act_backward": [C.c_int, _P, _P, _P, _P, _P, C.c_longlong, C.c_int, C.c_int, C.c_int, _P],
     "fr_bench_ffma": [C.c_int, C.c_int, C.c_int, _P, _P],
+    "fr_debug_tc_gemm_tf32": [_P, _P, _P, C.c_int, C.c_int, _P],
 }
 EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version", "fr_kernel_launches")
 
@@ -126,7 +127,7 @@ def lib():
 LAUNCHERS = frozenset({
     "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_jet_act_forward",
-    "fr_jet_act_backward", "fr_bench_ffma",
+    "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
 })
 launch_count = 0
 

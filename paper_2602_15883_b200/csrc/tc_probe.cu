@@ -1,0 +1,81 @@
+// Debug entry: one 128 x N x K TF32 GEMM through tcgen05 (TMEM accumulator),
+// C[128][N] = A[128][K] * B[N][K]^T.  Validates the UMMA descriptor / TMEM /
+// tcgen05.ld plumbing of tcgen05.cuh against a host matmul (tests/test_gpu_tc.py).
+#include "flowrec_b200.h"
+#include "jetmlp.cuh"
+#include "tcgen05.cuh"
+
+namespace fr {
+
+// k-quad staging: X[(k>>2)*(rows*4) + row*4 + (k&3)]
+__global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ C, int N, int K, int ncols) {
+  extern __shared__ __align__(128) float sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  float* As = sm;
+  float* Bs = sm + 128 * K;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 128 * K; i += 128) {
+    const int r = i / K, k = i % K;
+    As[(k >> 2) * 512 + r * 4 + (k & 3)] = A[i];
+  }
+  for (int i = tid; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = B[i];
+  }
+  if (warp == 0) {
+    // allocation width must be a power of two >= 32 columns
+    if (ncols <= 32) tc::tmem_alloc<32>(&tbase);
+    else if (ncols <= 64) tc::tmem_alloc<64>(&tbase);
+    else if (ncols <= 128) tc::tmem_alloc<128>(&tbase);
+    else tc::tmem_alloc<256>(&tbase);
+  }
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_tf32(128, N);
+    for (int kk = 0; kk < K / 8; ++kk) {
+      const uint64_t ad = tc::desc_kmajor(As + kk * 2 * 512, 512 * 4, 128);
+      const uint64_t bd = tc::desc_kmajor(Bs + kk * 2 * (N * 4), N * 16, 128);
+      tc::mma_tf32(tmem, ad, bd, idesc, kk > 0);
+    }
+    tc::mma_commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+    for (int i = 0; i < 16; ++i) C[row * N + c0 + i] = v[i];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    if (ncols <= 32) tc::tmem_free<32>(tmem);
+    else if (ncols <= 64) tc::tmem_free<64>(tmem);
+    else if (ncols <= 128) tc::tmem_free<128>(tmem);
+    else tc::tmem_free<256>(tmem);
+  }
+}
+
+}  // namespace fr
+
+extern "C" int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, fr_stream_t stream) {
+  if (N < 16 || N > 256 || N % 16 || K < 8 || K % 8 || K > 64) return -1;
+  const size_t smem = sizeof(float) * size_t(128 + N) * K;
+  if (cudaFuncSetAttribute(fr::tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      cudaSuccess)
+    return -2;
+  fr::tc_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, C, N, K, N);
+  ++fr::g_kernel_launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
