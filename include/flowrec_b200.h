@@ -44,6 +44,9 @@ enum { FR_STEADY2D = 0, FR_UNSTEADY2D = 1, FR_UNSTEADY3D = 2 };          /* phys
 enum { FR_F32 = 0, FR_F64 = 1 };
 enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3 };
 enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2 };
+/* contraction math of the training kernels: FP32 SIMT (oracle parity ~1e-5) or
+ * TF32 tcgen05 tensor cores (wide FP32 experts, 64 < width <= 512; default) */
+enum { FR_MATH_SIMT = 0, FR_MATH_TF32 = 1 };
 
 typedef struct {
   int n_in, n_out, n_vel, hidden_layers, width, width_pad;
@@ -52,6 +55,7 @@ typedef struct {
   int kp_elems;      /* elements of the prepared kernel-parameter buffer */
   int dtype, act, regime, num_sms;
   double inv_re;
+  int math;          /* FR_MATH_* of the PDE / MSE training kernels */
 } fr_plan_info;
 
 typedef struct {
@@ -64,7 +68,7 @@ typedef struct {
   long long scratch_bytes; /* per-call stash workspace */
   size_t smem_bytes;
   int loss_rows;           /* rows of 2 doubles in lpart (== grid for the fused kernels) */
-  int wide;                /* 1: layer-wise wide kernels (hidden width > 64) */
+  int wide;                /* 1: layer-wise SIMT wide kernels (hidden width > 64), 2: TF32 tcgen05 wide kernels */
 } fr_workspace;
 
 /* Plan: validated network + regime description (replaces per-bind checks). */
@@ -72,6 +76,8 @@ int fr_plan_create(const int* arch, int n_arch, int act, int regime, double inv_
                    fr_plan** out);
 int fr_plan_destroy(fr_plan* plan);
 int fr_plan_get_info(const fr_plan* plan, fr_plan_info* out);
+/* select FR_MATH_SIMT or FR_MATH_TF32 for the plan's PDE / MSE training kernels */
+int fr_plan_set_math(fr_plan* plan, int math);
 int fr_plan_workspace(const fr_plan* plan, int mode, long long n, fr_workspace* out);
 
 /* flat f64 params (reference layout) -> padded kernel params (+ W^T copies) */
@@ -176,8 +182,12 @@ int fr_jet_act_backward(int kind, const double* z, const double* s, const double
 int fr_bench_ffma(int grid, int iters, int unused, float* out, fr_stream_t stream);
 
 /* tcgen05 probe: C[128][N] = A[128][K] * B[N][K]^T in TF32 on the tensor core,
- * accumulator in TMEM (16 <= N <= 256, N % 16 == 0, K % 8 == 0, K <= 64) */
-int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, fr_stream_t stream);
+ * accumulator in TMEM (16 <= N <= 256, N % 16 == 0, K % 8 == 0, K <= 64);
+ * layout bit 0 / bit 1 stage A / B MN-major instead of K-major */
+int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, int layout, fr_stream_t stream);
+/* tcgen05 layout discovery: C[128][32] = words of A's shared tile (filled with
+ * their own indices) that one 128x32xK MMA reads under descriptor (lbo, sbo) */
+int fr_debug_tc_raw(float* C, int K, int a_mn, int lbo, int sbo, fr_stream_t stream);
 
 /* running count of kernels enqueued by this library (host-side counter) */
 long long fr_kernel_launches(void);

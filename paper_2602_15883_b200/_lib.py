@@ -32,7 +32,7 @@ class PlanInfo(C.Structure):
         ("hidden_layers", C.c_int), ("width", C.c_int), ("width_pad", C.c_int),
         ("n_params", C.c_int), ("np_pad", C.c_int), ("kp_elems", C.c_int),
         ("dtype", C.c_int), ("act", C.c_int), ("regime", C.c_int), ("num_sms", C.c_int),
-        ("inv_re", C.c_double),
+        ("inv_re", C.c_double), ("math", C.c_int),
     ]
 
 
@@ -74,6 +74,7 @@ _SIGS = {
     "fr_plan_create": [C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_P)],
     "fr_plan_destroy": [_P],
     "fr_plan_get_info": [_P, C.POINTER(PlanInfo)],
+    "fr_plan_set_math": [_P, C.c_int],
     "fr_plan_workspace": [_P, C.c_int, C.c_longlong, C.POINTER(Workspace)],
     "fr_prepare_params": [_P, _P, _P, _P],
     "fr_pde_fwd_bwd": [_P, _P, _P, C.c_longlong, C.c_double, _P, _P, _P, _P],
@@ -91,7 +92,8 @@ _SIGS = {
     "fr_jet_act_forward": [C.c_int, _P, _P, _P, _P, _P, C.c_longlong, C.c_int, C.c_int, _P],
     "fr_jet_act_backward": [C.c_int, _P, _P, _P, _P, _P, C.c_longlong, C.c_int, C.c_int, C.c_int, _P],
     "fr_bench_ffma": [C.c_int, C.c_int, C.c_int, _P, _P],
-    "fr_debug_tc_gemm_tf32": [_P, _P, _P, C.c_int, C.c_int, _P],
+    "fr_debug_tc_gemm_tf32": [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P],
+    "fr_debug_tc_raw": [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P],
 }
 EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version", "fr_kernel_launches")
 

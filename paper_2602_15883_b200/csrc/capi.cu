@@ -25,6 +25,7 @@ FR_DECL(mode_entry_JET)
 int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 int wide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int wide_entry_f64(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
+int tcwide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 }  // namespace fr
 
@@ -107,6 +108,10 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   I.n_in = din; I.n_out = nout; I.n_vel = nvel;
   I.hidden_layers = n_arch - 2; I.width = width; I.width_pad = wpad;
   I.dtype = dtype; I.act = act; I.regime = regime; I.inv_re = inv_re;
+  // wide FP32 experts train on the tcgen05 TF32 path by default (hidden
+  // contractions of >= 128 units are real dense GEMMs); fr_plan_set_math
+  // switches back to FP32 SIMT
+  I.math = (dtype == FR_F32 && wpad > 64 && wpad <= 512) ? FR_MATH_TF32 : FR_MATH_SIMT;
   const int L = I.hidden_layers;
   p->pl = ParamLayout{din, wpad, nout, L};
   I.np_pad = p->pl.np_pad();
@@ -167,6 +172,21 @@ extern "C" int fr_plan_destroy(fr_plan* p) {
   return 0;
 }
 
+extern "C" int fr_plan_set_math(fr_plan* p, int math) {
+  if (!p) return fail("fr_plan_set_math: NULL plan");
+  if (math == FR_MATH_SIMT) {
+    p->info.math = math;
+    return 0;
+  }
+  if (math != FR_MATH_TF32) return fail("unknown math mode %d", math);
+  const fr_plan_info& I = p->info;
+  if (I.dtype != FR_F32) return fail("TF32 tensor-core math needs an FP32 plan");
+  if (I.width_pad <= 64 || I.width_pad > 512)
+    return fail("TF32 tensor-core math covers hidden widths 65..512 (got %d)", I.width);
+  p->info.math = math;
+  return 0;
+}
+
 extern "C" int fr_plan_get_info(const fr_plan* p, fr_plan_info* out) {
   if (!p || !out) return fail("fr_plan_get_info: NULL argument");
   *out = p->info;
@@ -209,14 +229,21 @@ static int epoch_call(const fr_plan* p, const EpochArgs* e, int grid, cudaStream
   return 0;
 }
 
-constexpr int WIDE_KS = 32;  // gradient-partial rows (row splits) of the wide kernels
+constexpr int WIDE_KS = 32;  // gradient-partial rows (row splits) of the SIMT wide kernels
+constexpr int TC_KS = 64;    // ... of the tensor-core wide kernels
 
 static bool is_wide(const fr_plan* p) { return p->info.width_pad > 64; }
+// training heads of TF32 plans run on the tcgen05 kernels (prediction stays SIMT)
+static bool is_tc(const fr_plan* p, int mode) {
+  return is_wide(p) && p->info.math == FR_MATH_TF32 && (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+}
+static int wide_ks(const fr_plan* p, int mode) { return is_tc(p, mode) ? TC_KS : WIDE_KS; }
 
 static int wide_call(const fr_plan* p, int mode, const WArgs* a, cudaStream_t st, WInfo* wi) {
   const fr_plan_info& I = p->info;
-  const int r = I.dtype == FR_F32 ? wide_entry_f32(mode, I.act, I.regime, a, WIDE_KS, st, wi)
-                                  : wide_entry_f64(mode, I.act, I.regime, a, WIDE_KS, st, wi);
+  const int r = is_tc(p, mode) ? tcwide_entry_f32(mode, I.act, I.regime, a, TC_KS, st, wi)
+                : I.dtype == FR_F32 ? wide_entry_f32(mode, I.act, I.regime, a, WIDE_KS, st, wi)
+                                    : wide_entry_f64(mode, I.act, I.regime, a, WIDE_KS, st, wi);
   if (r == -1) return fail("wide kernel variant not compiled");
   if (r != 0) return cuda_fail(cudaError_t(r), "wide kernel launch");
   return 0;
@@ -232,7 +259,7 @@ static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WIn
   z->ntiles = (n + wi->ppt - 1) / wi->ppt;
   z->act = L * z->ntiles * WP * wi->rows;
   const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
-  z->stash = bwd ? L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt : 0;
+  z->stash = bwd ? L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt : 0;  // 0 on the TF32 path
   z->ybar = bwd ? z->ntiles * wi->rows * I.n_out : 0;
   auto al = [](long long e) { return (e + 63) / 64 * 64; };
   z->total = al(z->act) + (bwd ? al(z->act) : 0) + al(z->stash) + al(z->ybar);
@@ -248,16 +275,17 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
     if (wide_sizes(p, mode, n, &z, &wi)) return 1;
     const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
     const size_t esz = p->info.dtype == FR_F32 ? 4 : 8;
-    out->grid = WIDE_KS;
+    const int ks = wide_ks(p, mode);
+    out->grid = ks;
     out->threads = wi.nt;
     out->points_per_tile = wi.ppt;
     out->jet_streams = 1 + 2 * p->info.n_in;
-    out->gpart_elems = bwd ? (long long)WIDE_KS * p->info.np_pad : 0;
+    out->gpart_elems = bwd ? (long long)ks * p->info.np_pad : 0;
     out->lpart_elems = bwd ? z.ntiles * 2 : 0;
     out->loss_rows = bwd ? int(z.ntiles) : 0;
     out->scratch_bytes = z.total * (long long)esz;
     out->smem_bytes = 0;
-    out->wide = 1;
+    out->wide = is_tc(p, mode) ? 2 : 1;
     return 0;
   }
   KInfo ki{};
@@ -312,9 +340,9 @@ static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* 
   a.L = I.hidden_layers;
   a.WP = I.width_pad;
   a.np_pad = I.np_pad;
-  a.ks_rows = WIDE_KS;
+  a.ks_rows = wide_ks(p, mode);
   a.inv_re = I.inv_re;
-  if (bwd) FR_CUDA(cudaMemsetAsync(a.gpart, 0, sizeof(double) * size_t(WIDE_KS) * I.np_pad, st), "gpart zero");
+  if (bwd) FR_CUDA(cudaMemsetAsync(a.gpart, 0, sizeof(double) * size_t(a.ks_rows) * I.np_pad, st), "gpart zero");
   const int r = wide_call(p, mode, &a, st, nullptr);
   if (owned) cudaFreeAsync(owned, st);
   return r;

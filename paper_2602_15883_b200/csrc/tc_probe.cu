@@ -8,8 +8,9 @@
 namespace fr {
 
 // k-quad staging: X[(k>>2)*(rows*4) + row*4 + (k&3)]
+// layout bit 0: A MN-major, bit 1: B MN-major
 __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__ A, const float* __restrict__ B,
-                                                      float* __restrict__ C, int N, int K, int ncols) {
+                                                      float* __restrict__ C, int N, int K, int ncols, int layout) {
   extern __shared__ __align__(128) float sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tbase;
@@ -18,11 +19,13 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 128 * K; i += 128) {
     const int r = i / K, k = i % K;
-    As[(k >> 2) * 512 + r * 4 + (k & 3)] = A[i];
+    if (layout & 1) As[(r >> 2) * (K * 4) + k * 4 + (r & 3)] = A[i];
+    else As[(k >> 2) * 512 + r * 4 + (k & 3)] = A[i];
   }
   for (int i = tid; i < N * K; i += 128) {
     const int r = i / K, k = i % K;
-    Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = B[i];
+    if (layout & 2) Bs[(r >> 2) * (K * 4) + k * 4 + (r & 3)] = B[i];
+    else Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = B[i];
   }
   if (warp == 0) {
     // allocation width must be a power of two >= 32 columns
@@ -41,10 +44,12 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__
   tc::fence_after();
   const uint32_t tmem = tbase;
   if (tid == 0) {
-    const uint32_t idesc = tc::idesc_tf32(128, N);
+    const uint32_t idesc = tc::idesc_tf32(128, N, layout & 1, (layout >> 1) & 1);
     for (int kk = 0; kk < K / 8; ++kk) {
-      const uint64_t ad = tc::desc_kmajor(As + kk * 2 * 512, 512 * 4, 128);
-      const uint64_t bd = tc::desc_kmajor(Bs + kk * 2 * (N * 4), N * 16, 128);
+      // K-major: LBO = K-chunk stride, SBO = 8-row stride; MN-major: LBO = 8-k stride, SBO = 4-row group stride
+      const uint64_t ad = (layout & 1) ? tc::desc(As + kk * 32, 128, K * 16) : tc::desc(As + kk * 2 * 512, 512 * 4, 128);
+      const uint64_t bd = (layout & 2) ? tc::desc(Bs + kk * 32, 128, K * 16)
+                                       : tc::desc(Bs + kk * 2 * (N * 4), N * 16, 128);
       tc::mma_tf32(tmem, ad, bd, idesc, kk > 0);
     }
     tc::mma_commit(&mbar);
@@ -69,13 +74,67 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__
 
 }  // namespace fr
 
-extern "C" int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, fr_stream_t stream) {
+extern "C" int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, int layout,
+                                     fr_stream_t stream) {
   if (N < 16 || N > 256 || N % 16 || K < 8 || K % 8 || K > 64) return -1;
   const size_t smem = sizeof(float) * size_t(128 + N) * K;
   if (cudaFuncSetAttribute(fr::tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess)
     return -2;
-  fr::tc_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, C, N, K, N);
+  fr::tc_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, C, N, K, N, layout);
+  ++fr::g_kernel_launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// Layout discovery: A smem filled with its own word indices, B = identity
+// (K-major), so C[m][k] reveals which shared-memory word the tensor core read
+// for A(m, k) under the given descriptor strides (a_mn selects MN-major).
+namespace fr {
+__global__ void __launch_bounds__(128) tc_raw_kernel(float* __restrict__ C, int K, int a_mn, int lbo, int sbo) {
+  extern __shared__ __align__(128) float sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  constexpr int N = 32;
+  float* As = sm;
+  float* Bs = sm + 128 * K;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 128 * K; i += 128) As[i] = float(i);
+  for (int i = tid; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = (r == k) ? 1.f : 0.f;
+  }
+  if (warp == 0) tc::tmem_alloc<32>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    tc::mma_tf32(tmem, tc::desc(As, lbo, sbo), tc::desc(Bs, N * 16, 128), tc::idesc_tf32(128, N, a_mn, 0), 0);
+    tc::mma_commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+    for (int i = 0; i < 16; ++i) C[row * N + c0 + i] = v[i];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<32>(tmem);
+}
+}  // namespace fr
+
+extern "C" int fr_debug_tc_raw(float* C, int K, int a_mn, int lbo, int sbo, fr_stream_t stream) {
+  const size_t smem = sizeof(float) * size_t(128 + 32) * K;
+  cudaFuncSetAttribute(fr::tc_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  fr::tc_raw_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(C, K, a_mn, lbo, sbo);
   ++fr::g_kernel_launches;
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

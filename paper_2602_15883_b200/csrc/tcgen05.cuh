@@ -18,8 +18,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// UMMA shared-memory descriptor (K-major, SWIZZLE_NONE, sm_100 version 1)
-__device__ __forceinline__ uint64_t desc_kmajor(const void* smem, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// UMMA shared-memory descriptor (SWIZZLE_NONE, sm_100 version 1).  K-major:
+// LBO = stride between 16-byte K chunks, SBO = stride between 8-row groups.
+// MN-major: LBO = stride between 8-deep K groups, SBO = stride between 16-byte
+// (4-element) MN groups; a core matrix is 8 K rows x 16 bytes of MN.
+__device__ __forceinline__ uint64_t desc(const void* smem, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= uint64_t((smem_u32(smem) >> 4) & 0x3FFF);
   d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
@@ -29,13 +32,13 @@ __device__ __forceinline__ uint64_t desc_kmajor(const void* smem, uint32_t lbo_b
   return d;
 }
 
-// instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M x N
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+// instruction descriptor: kind::tf32, D f32, M x N; a_mn / b_mn select MN-major operands
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)            // c_format = F32
          | (2u << 7)          // a_format = TF32
          | (2u << 10)         // b_format = TF32
-         | (0u << 15)         // a_major = K
-         | (0u << 16)         // b_major = K
+         | (uint32_t(a_mn & 1) << 15)  // a_major
+         | (uint32_t(b_mn & 1) << 16)  // b_major
          | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
@@ -71,6 +74,19 @@ __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t phase) {
         : "r"(a), "r"(phase)
         : "memory");
   }
+}
+
+// arrive on an mbarrier announcing `bytes` of incoming async-copy traffic
+__device__ __forceinline__ void mbar_expect_tx(void* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA engine), completes `bytes` on mbar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, void* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
 }
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }

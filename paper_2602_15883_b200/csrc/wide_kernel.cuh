@@ -93,6 +93,11 @@ struct WArgs {
   double coef, pcoef, inv_re;
   double velw[4];
   int has_p;
+  // tensor-core path only
+  long long tcw_f, tcw_d;  // kp offsets of the K-major operand slabs of W_l for fwd (N = out) / dx (N = in)
+  int nb;                 // output units per CTA (N of the MMA)
+  float* p0;              // [tiles][(DIN+1)*WP] per-tile dW_0 | db_0 partials
+  float* pL;              // [tiles][WP*NOUT + NOUT] per-tile dW_L | db_L partials
 };
 
 template <typename C>

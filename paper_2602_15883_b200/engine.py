@@ -30,10 +30,16 @@ def require_cuda():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+MATH_CODES = {"simt": 0, "tf32": 1}
+
+
 class Plan:
     """A validated (architecture, activation, regime, dtype) for the kernels."""
 
-    def __init__(self, config, regime_kind, reynolds, dtype="float32"):
+    def __init__(self, config, regime_kind, reynolds, dtype="float32", math=None):
+        """`math`: None keeps the library default (TF32 tensor cores for FP32
+        experts wider than 64 units, FP32 SIMT otherwise); "simt" / "tf32"
+        force the contraction math of the PDE / MSE training kernels."""
         self.device = require_cuda()
         self.config = config
         self.regime_kind = regime_kind
@@ -45,6 +51,10 @@ class Plan:
         X.call("fr_plan_create", carr, len(arch), X.ACT_CODES[config.activation],
                X.REGIME_CODES[regime_kind], 1.0 / float(reynolds), self.code, C.byref(h))
         self.h = h
+        if math is not None:
+            if math not in MATH_CODES:
+                raise ValueError(f"unknown math {math!r}; expected one of {sorted(MATH_CODES)}")
+            X.call("fr_plan_set_math", h, MATH_CODES[math])
         info = X.PlanInfo()
         X.call("fr_plan_get_info", h, C.byref(info))
         self.info = info
@@ -68,12 +78,12 @@ _plans = {}
 _plans_lock = threading.Lock()
 
 
-def get_plan(config, regime_kind, reynolds, dtype="float32"):
-    key = (config, regime_kind, float(reynolds), dtype_code(dtype), torch.cuda.current_device())
+def get_plan(config, regime_kind, reynolds, dtype="float32", math=None):
+    key = (config, regime_kind, float(reynolds), dtype_code(dtype), math, torch.cuda.current_device())
     with _plans_lock:
         p = _plans.get(key)
         if p is None:
-            p = Plan(config, regime_kind, reynolds, dtype)
+            p = Plan(config, regime_kind, reynolds, dtype, math)
             _plans[key] = p
         return p
 

@@ -239,14 +239,14 @@ class LocalObjective:
     is a float64 numpy vector in the reference's flat layout.
     """
 
-    def __init__(self, config, regime, datasets, weights, batch_size, dtype="float32"):
+    def __init__(self, config, regime, datasets, weights, batch_size, dtype="float32", math=None):
         if batch_size < 1:
             raise ValueError("batch size must be >= 1")
         self.config = config
         self.regime = regime
         self.weights = weights
         self.batch = int(batch_size)
-        self.plan = get_plan(config, regime.kind, regime.reynolds, dtype)
+        self.plan = get_plan(config, regime.kind, regime.reynolds, dtype, math)
         self.dev = DeviceObjective(self.plan, regime, datasets, weights)
         self.n_obs, self.n_colloc = self.dev.n_obs, self.dev.n_colloc
         self.n_ghost, self.n_ghost_total = self.dev.n_ghost, self.dev.n_ghost_total

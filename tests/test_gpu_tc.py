@@ -15,8 +15,9 @@ def _tf32(x):
     return (b & np.uint32(0xFFFFE000)).view(np.float32)
 
 
+@pytest.mark.parametrize("layout", [0, 1, 2, 3])
 @pytest.mark.parametrize("N,K", [(16, 8), (64, 32), (128, 64), (256, 64), (96, 40)])
-def test_tc_gemm_tf32(N, K):
+def test_tc_gemm_tf32(N, K, layout):
     import torch
 
     from paper_2602_15883_b200 import _lib as X
@@ -27,7 +28,7 @@ def test_tc_gemm_tf32(N, K):
     dA = torch.from_numpy(A).cuda()
     dB = torch.from_numpy(B).cuda()
     dC = torch.zeros((128, N), dtype=torch.float32, device="cuda")
-    X.call("fr_debug_tc_gemm_tf32", dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), N, K, None)
+    X.call("fr_debug_tc_gemm_tf32", dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), N, K, layout, None)
     torch.cuda.synchronize()
     C = dC.cpu().numpy().astype(np.float64)
     ref = _tf32(A).astype(np.float64) @ _tf32(B).astype(np.float64).T
