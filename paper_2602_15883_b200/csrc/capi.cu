@@ -61,7 +61,9 @@ struct fr_plan {
   fr_plan_info info;
   ParamLayout pl;
   int* d_map = nullptr;      // real flat index -> padded index      [n_params]
-  int* d_mapT = nullptr;     // real flat index -> W^T copy index or -1 [n_params]
+  int* d_mapT = nullptr;     // real flat index -> {W^T copy, fwd slab, dx slab} indices or -1 [3 * n_params]
+  long long tcw_f = 0, tcw_d = 0;  // kp offsets of the tensor-core operand slabs (0: none)
+  int tc_nb = 0;                   // N of the tensor-core MMAs (output units per CTA)
   int* d_inv = nullptr;      // kernel-param element -> real index or -1 [kp_elems]
 };
 
@@ -108,14 +110,31 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   I.n_in = din; I.n_out = nout; I.n_vel = nvel;
   I.hidden_layers = n_arch - 2; I.width = width; I.width_pad = wpad;
   I.dtype = dtype; I.act = act; I.regime = regime; I.inv_re = inv_re;
-  // wide FP32 experts train on the tcgen05 TF32 path by default (hidden
-  // contractions of >= 128 units are real dense GEMMs); fr_plan_set_math
-  // switches back to FP32 SIMT
-  I.math = (dtype == FR_F32 && wpad > 64 && wpad <= 512) ? FR_MATH_TF32 : FR_MATH_SIMT;
   const int L = I.hidden_layers;
   p->pl = ParamLayout{din, wpad, nout, L};
   I.np_pad = p->pl.np_pad();
   I.kp_elems = p->pl.total();
+  // tensor-core operand slabs of the hidden weights (FP32 wide experts): per
+  // layer, per N block of NB units, per 16-deep K chunk, a contiguous K-major
+  // [4 quads][NB][4] slab -- one for the forward (N = out units, K = in units)
+  // and one for the adjoint (N = in units, K = out units)
+  const bool tc_ok = dtype == FR_F32 && wpad > 64 && wpad <= 512 && I.hidden_layers >= 2;
+  const int tc_nb = wpad <= 256 ? wpad : wpad / 2;
+  if (tc_ok) {
+    p->tc_nb = tc_nb;
+    p->tcw_f = (I.kp_elems + 3) & ~3;
+    p->tcw_d = p->tcw_f + (long long)(I.hidden_layers - 1) * wpad * wpad;
+    I.kp_elems = int(p->tcw_d + (long long)(I.hidden_layers - 1) * wpad * wpad);
+  }
+  // wide FP32 experts train on the tcgen05 TF32 path by default (hidden
+  // contractions of >= 128 units are real dense GEMMs); fr_plan_set_math
+  // switches back to FP32 SIMT
+  I.math = tc_ok ? FR_MATH_TF32 : FR_MATH_SIMT;
+  auto tc_slab = [&](long long base, int l, int n_unit, int k_unit) -> int {
+    const int nnb = wpad / tc_nb, nch = wpad / 16;
+    const int nb = n_unit / tc_nb, n = n_unit % tc_nb, c = k_unit / 16, kq = (k_unit % 16) / 4, j = k_unit % 4;
+    return int(base + ((long long)((l - 1) * nnb + nb) * nch + c) * tc_nb * 16 + kq * tc_nb * 4 + n * 4 + j);
+  };
   // real flat layout W0,b0,W1,b1,... (network.py:112-115)
   std::vector<int> map, mapT;
   std::vector<int> inv(I.kp_elems, -1);
@@ -127,19 +146,27 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
       for (int o = 0; o < fo; ++o) {
         const int pidx = p->pl.off_w(l) + i * fo_pad + o;
         inv[pidx] = int(map.size());
-        int tidx = -1;
+        int tidx = -1, fidx = -1, didx = -1;
         if (l >= 1 && l < L) {
           tidx = p->pl.off_wt(l) + o * wpad + i;
           inv[tidx] = int(map.size());
+          if (tc_ok) {
+            fidx = tc_slab(p->tcw_f, l, o, i);
+            didx = tc_slab(p->tcw_d, l, i, o);
+            inv[fidx] = int(map.size());
+            inv[didx] = int(map.size());
+          }
         }
         map.push_back(pidx);
         mapT.push_back(tidx);
+        mapT.push_back(fidx);
+        mapT.push_back(didx);
       }
     for (int o = 0; o < fo; ++o) {
       const int pidx = p->pl.off_b(l) + o;
       inv[pidx] = int(map.size());
       map.push_back(pidx);
-      mapT.push_back(-1);
+      for (int r = 0; r < 3; ++r) mapT.push_back(-1);
     }
   }
   I.n_params = int(map.size());
@@ -181,8 +208,9 @@ extern "C" int fr_plan_set_math(fr_plan* p, int math) {
   if (math != FR_MATH_TF32) return fail("unknown math mode %d", math);
   const fr_plan_info& I = p->info;
   if (I.dtype != FR_F32) return fail("TF32 tensor-core math needs an FP32 plan");
-  if (I.width_pad <= 64 || I.width_pad > 512)
-    return fail("TF32 tensor-core math covers hidden widths 65..512 (got %d)", I.width);
+  if (p->tc_nb == 0)
+    return fail("TF32 tensor-core math covers hidden widths 65..512 with >= 2 hidden layers (got %d x %d)", I.width,
+                I.hidden_layers);
   p->info.math = math;
   return 0;
 }
@@ -230,12 +258,12 @@ static int epoch_call(const fr_plan* p, const EpochArgs* e, int grid, cudaStream
 }
 
 constexpr int WIDE_KS = 32;  // gradient-partial rows (row splits) of the SIMT wide kernels
-constexpr int TC_KS = 64;    // ... of the tensor-core wide kernels
+constexpr int TC_KS = 128;   // ... of the tensor-core wide kernels
 
 static bool is_wide(const fr_plan* p) { return p->info.width_pad > 64; }
 // training heads of TF32 plans run on the tcgen05 kernels (prediction stays SIMT)
 static bool is_tc(const fr_plan* p, int mode) {
-  return is_wide(p) && p->info.math == FR_MATH_TF32 && (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  return is_wide(p) && p->tc_nb > 0 && p->info.math == FR_MATH_TF32 && (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
 }
 static int wide_ks(const fr_plan* p, int mode) { return is_tc(p, mode) ? TC_KS : WIDE_KS; }
 
@@ -259,8 +287,14 @@ static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WIn
   z->ntiles = (n + wi->ppt - 1) / wi->ppt;
   z->act = L * z->ntiles * WP * wi->rows;
   const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
-  z->stash = bwd ? L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt : 0;  // 0 on the TF32 path
-  z->ybar = bwd ? z->ntiles * wi->rows * I.n_out : 0;
+  // SIMT: activation stash; tensor cores: row-quad-major S_l and Zbar_l copies
+  z->stash = !bwd ? 0
+             : is_tc(p, mode) ? 2 * L * z->ntiles * WP * 128
+                              : L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt;
+  // SIMT: Ybar rows; tensor cores: per-tile dW_0|db_0 and dW_L|db_L partials
+  z->ybar = !bwd ? 0
+            : is_tc(p, mode) ? z->ntiles * ((I.n_in + 1) * WP + WP * I.n_out + I.n_out)
+                             : z->ntiles * wi->rows * I.n_out;
   auto al = [](long long e) { return (e + 63) / 64 * 64; };
   z->total = al(z->act) + (bwd ? al(z->act) : 0) + al(z->stash) + al(z->ybar);
   return 0;
@@ -341,6 +375,15 @@ static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* 
   a.WP = I.width_pad;
   a.np_pad = I.np_pad;
   a.ks_rows = wide_ks(p, mode);
+  if (is_tc(p, mode)) {
+    a.tcw_f = p->tcw_f;
+    a.tcw_d = p->tcw_d;
+    a.nb = p->tc_nb;
+    a.p0 = static_cast<float*>(a.ybar);
+    a.pL = a.p0 + size_t(z.ntiles) * (I.n_in + 1) * a.WP;
+    a.st = static_cast<float*>(a.stash);
+    a.zt = a.st + size_t(a.L) * z.ntiles * a.WP * 128;
+  }
   a.inv_re = I.inv_re;
   if (bwd) FR_CUDA(cudaMemsetAsync(a.gpart, 0, sizeof(double) * size_t(a.ks_rows) * I.np_pad, st), "gpart zero");
   const int r = wide_call(p, mode, &a, st, nullptr);
@@ -706,7 +749,9 @@ __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, co
     if (a.kparams) {
       T* kp = static_cast<T*>(a.kparams);
       kp[map[i]] = T(p);
-      if (mapT[i] >= 0) kp[mapT[i]] = T(p);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        if (mapT[3 * i + r] >= 0) kp[mapT[3 * i + r]] = T(p);
     }
   }
   // ---- the last block advances the step counter ----

@@ -1,5 +1,7 @@
 // TF32 tensor-core wide-expert training kernels (PDE and MSE heads), FP32 I/O.
 #include "jetmlp_dispatch.cuh"
+#include <algorithm>
+
 #include "tcwide_kernel.cuh"
 
 namespace fr {
@@ -15,23 +17,35 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   }
   if (!ap) return 0;
   const WArgs& a = *ap;
-  const int NB = a.WP <= 256 ? a.WP : a.WP / 2;
+  const int NB = a.nb;
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(tcw_fwd_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
     cudaFuncSetAttribute(tcw_dx_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
-    cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::dw_smem(256)));
+    cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tcw_head_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::head_smem(512)));
     attrs = true;
   }
   const dim3 gt(a.ntiles, a.WP / NB);
-  for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, C::NT, C::gemm_smem(NB), st>>>(a, l, NB);
+  for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, C::NT, C::gemm_smem(NB), st>>>(a, l);
   tcw_head_kernel<ACT, MODE, REG><<<a.ntiles, C::NT, C::head_smem(a.WP), st>>>(a);
-  for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, C::NT, C::gemm_smem(NB), st>>>(a, l, NB);
-  const dim3 gw((a.WP + 127) / 128, a.WP / NB, ks);
-  for (int l = a.L - 1; l >= 1; --l) tcw_dw_kernel<ACT, MODE, REG><<<gw, C::DW_NT, C::dw_smem(NB), st>>>(a, l, NB);
-  tcw_dwL_kernel<ACT, MODE, REG><<<ks, 128, 0, st>>>(a);
-  tcw_dw0_kernel<ACT, MODE, REG><<<dim3(ks, (a.WP + 127) / 128), 128, 0, st>>>(a);
+  for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, C::NT, C::gemm_smem(NB), st>>>(a, l);
+  // dW: all ceil(WP/128) k-blocks of an N block accumulate in TMEM (<= 512
+  // columns); N block = the largest multiple of 16 dividing WP that fits
+  const int nkb = (a.WP + 127) / 128;
+  int nbw = std::min(256, 512 / nkb) / 16 * 16;
+  while (a.WP % nbw) nbw -= 16;
+  const size_t stage = C::dw_stage_bytes(a.WP, nbw);
+  const int ns = int(std::min<size_t>(TC_DW_MAXNS, (200 * 1024) / stage));
+  const int splits = std::max(1, std::min(ks, 148 / (a.WP / nbw)));
+  const dim3 gw(a.WP / nbw, splits);
+  for (int l = a.L - 1; l >= 1; --l)
+    tcw_dw_kernel<ACT, MODE, REG><<<gw, C::DW_NT, stage * ns, st>>>(a, l, nbw, ns);
+  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
+  const int len0 = (C::DIN + 1) * a.WP, lenL = a.WP * C::NOUT + C::NOUT;
+  tcw_partials_kernel<<<dim3((len0 + 255) / 256, ks), 256, 0, st>>>(a.p0, len0, a.ntiles, a.gpart, a.np_pad, pl.off_w(0));
+  tcw_partials_kernel<<<dim3((lenL + 255) / 256, ks), 256, 0, st>>>(a.pL, lenL, a.ntiles, a.gpart, a.np_pad,
+                                                                      pl.off_w(a.L));
   g_kernel_launches += 3 * (a.L - 1) + 3;
   return int(cudaGetLastError());
 }

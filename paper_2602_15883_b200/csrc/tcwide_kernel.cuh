@@ -15,16 +15,25 @@
 // tile = 2 KB contiguous = a K-major 128 x 4 operand slab):
 //   Z    pre-activation jets of layers 1..L-1 (layer 0 is recomputed from the
 //        points on the fly: z_v = x W0 + b0, z_g = W0 rows, z_l = 0)
-//   Zbar their adjoints, layers 0..L-1
-//   ybar output-layer adjoints [tile][128][NOUT]
+//   Zbar their adjoints, layers 1..L-1 (Zbar_0 only feeds dW_0, which the
+//        layer-1 adjoint kernel reduces per tile without storing it)
+//   p0 / pL per-tile dW_0|db_0 and dW_L|db_L partials, reduced over tiles in a
+//        fixed order by tcw_partials_kernel
 // The activation sigma(Z) is applied by the CONSUMER (the next layer's operand
-// staging, the head, and the dW staging) so only Z is ever written:
-// fwd moves 2 x 128 x WP x 4 B per tile-layer instead of 3.
+// staging, the head, the dW staging), so the forward writes only Z.
+//
+// Data movement: every operand slab is fetched with 1-D bulk async copies
+// (cp.async.bulk, TMA engine) issued by one thread into a multi-stage
+// shared-memory ring with mbarrier transaction counts; the tensor core frees a
+// stage through tcgen05.commit on the stage's "empty" barrier.
 #pragma once
 #include "tcgen05.cuh"
 #include "wide_kernel.cuh"
 
 namespace fr {
+
+constexpr int TC_NS = 4;   // fwd / dx / head ring stages
+constexpr int TC_KC = 16;  // K depth of one stage (4 unit quads)
 
 template <int ACT, int MODE, int REG>
 struct TcCfg {
@@ -33,22 +42,21 @@ struct TcCfg {
   static constexpr int DIN = R::DIN, NOUT = R::NOUT, NVEL = R::NVEL;
   static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0;
   static constexpr bool JET = St::JET;
-  static constexpr int SIN = (ACT == ACT_SIN) ? 1 : 0;
   static constexpr int NT = 128;              // fwd / dx / head CTAs (one thread per TMEM lane)
-  static constexpr int DW_NT = 256;           // dW CTAs
+  static constexpr int DW_NT = 320;           // dW CTAs (loader, MMA, 8 drain / db warps)
   static constexpr int PPW = 32 / S;          // points per 32-row group
   static constexpr int PPT = 4 * PPW;         // points per tile
   static constexpr int VR = PPW * S;          // valid rows per 32-row group
-  static constexpr int KC = 32, NQ = KC / 4;  // K chunk = 8 quads
-  static constexpr int QS = NT / PPT;         // head: threads per point
-  static constexpr int ZRS = 32 * 4 + 4;      // dW Z staging row stride (words, conflict-free)
+  static constexpr int ITEMS = PPT * 4;       // (point, unit quad) items of one 16-deep chunk
+  static constexpr int TPP = ITEMS <= NT ? 4 : 1;  // threads holding partial sums of one point (head)
   __host__ __device__ static constexpr int row0(int pt) { return (pt / PPW) * 32 + (pt % PPW) * S; }
-  __host__ __device__ static size_t gemm_smem(int NB) { return sizeof(float) * size_t(2 * NQ * 512 + 2 * NQ * NB * 4); }
-  __host__ __device__ static size_t dw_smem(int NB) {
-    return sizeof(float) * size_t(32 * ZRS + 2 * 8 * 128 * 4 + 2 * 8 * NB * 4);
-  }
+  __host__ __device__ static constexpr size_t stage_floats(int NB) { return 2048 + size_t(NB) * 16; }
+  __host__ __device__ static size_t gemm_smem(int NB) { return sizeof(float) * TC_NS * stage_floats(NB); }
+  __host__ __device__ static size_t dw_stage_bytes(int WP, int NB) { return size_t(WP + NB) * 128; }
+  static constexpr int HEAD_RED = PPT * 16 * NOUT;  // [pt][kq][j][o]
   __host__ __device__ static size_t head_smem(int WP) {
-    return sizeof(float) * size_t(WP * NOUT + PPT * QS * S * NOUT + 2 * PPT * S * NOUT) + 2 * NT * sizeof(double);
+    return sizeof(double) * 2 * NT +
+           sizeof(float) * size_t(TC_NS * 2048 + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
   }
 };
 
@@ -56,34 +64,27 @@ __device__ __forceinline__ size_t tc_off(const WArgs& a, int l, long long tile, 
   return ((size_t(l) * a.ntiles + tile) * (a.WP / 4) + q) * 512;
 }
 
-// pre-activation jets of point pt (tile-local), unit quad q, of hidden layer l
+// layer-0 pre-activation jets of point p (global index), units 4q..4q+3
 template <class C>
-__device__ __forceinline__ void tc_load_z(const WArgs& a, const float* __restrict__ kp, const ParamLayout& pl,
-                                          int l, long long tile, int pt, int q, float (&z)[C::S][4]) {
-  if (l == 0) {
-    const long long p = tile * C::PPT + pt;
-    const float* pts = static_cast<const float*>(a.pts);
-    float x[C::DIN];
+__device__ __forceinline__ void tc_z0(const WArgs& a, const float* __restrict__ kp, const ParamLayout& pl,
+                                      long long p, int q, float (&z)[C::S][4]) {
+  const float* pts = static_cast<const float*>(a.pts);
+  float x[C::DIN];
 #pragma unroll
-    for (int i = 0; i < C::DIN; ++i) x[i] = p < a.n ? pts[p * C::DIN + i] : 0.f;
+  for (int i = 0; i < C::DIN; ++i) x[i] = p < a.n ? pts[p * C::DIN + i] : 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int u = 4 * q + j;
-      float zv = 0.f;
+  for (int j = 0; j < 4; ++j) {
+    const int u = 4 * q + j;
+    float zv = 0.f;
 #pragma unroll
-      for (int i = 0; i < C::DIN; ++i) zv = fmaf(x[i], kp[pl.off_w(0) + i * a.WP + u], zv);
-      z[0][j] = zv + kp[pl.off_b(0) + u];
-      if constexpr (C::JET) {
+    for (int i = 0; i < C::DIN; ++i) zv = fmaf(x[i], kp[pl.off_w(0) + i * a.WP + u], zv);
+    z[0][j] = zv + kp[pl.off_b(0) + u];
+    if constexpr (C::JET) {
 #pragma unroll
-        for (int i = 0; i < C::NG; ++i) z[1 + i][j] = kp[pl.off_w(0) + i * a.WP + u];
+      for (int i = 0; i < C::NG; ++i) z[1 + i][j] = kp[pl.off_w(0) + i * a.WP + u];
 #pragma unroll
-        for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i][j] = 0.f;
-      }
+      for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i][j] = 0.f;
     }
-  } else {
-    const float* b = static_cast<const float*>(a.act) + tc_off(a, l, tile, q) + C::row0(pt) * 4;
-#pragma unroll
-    for (int s = 0; s < C::S; ++s) vload(z[s], b + 4 * s);
   }
 }
 
@@ -105,14 +106,23 @@ __device__ __forceinline__ void tc_act1(const float (&z)[C::S], float (&s)[C::S]
   }
 }
 
-// activation adjoint of one point / unit (in place: sb = S-bar -> Z-bar)
+// activation adjoint of one point / unit (in place: sb = S-bar -> Z-bar);
+// also returns the forward activation in sa (for the weight gradient)
 template <class C, int ACT>
-__device__ __forceinline__ void tc_act_bwd1(const float (&z)[C::S], float (&sb)[C::S]) {
+__device__ __forceinline__ void tc_act_bwd1(const float (&z)[C::S], float (&sb)[C::S], float (&sa)[C::S]) {
   constexpr int NG = C::NG, NL = C::NL, LAP0 = C::LAP0;
   float s, c, d1, d2;
   act_eval<ACT>(z[0], s, c);
   act_d12<ACT>(s, c, d1, d2);
+  sa[0] = s;
   if constexpr (C::JET) {
+#pragma unroll
+    for (int i = 0; i < NG; ++i) sa[1 + i] = d1 * z[1 + i];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      const float zg = z[1 + LAP0 + i];
+      sa[1 + NG + i] = d2 * zg * zg + d1 * z[1 + NG + i];
+    }
     const float d3 = act_d3<ACT>(s, c, d1, d2);
     float zv = sb[0] * d1;
 #pragma unroll
@@ -139,32 +149,55 @@ __device__ __forceinline__ void tc_act_bwd1(const float (&z)[C::S], float (&sb)[
   }
 }
 
-template <class C, int ACT>
-__device__ __forceinline__ void tc_act4(const float (&z)[C::S][4], float (&s)[C::S][4]) {
+// the S rows x 4 units of item (pt, kq) in a [kq][128][4] slab
+template <class C>
+__device__ __forceinline__ void slab_load(float (&v)[C::S][4], const float* slab, int pt, int kq) {
+  const float* b = slab + kq * 512 + C::row0(pt) * 4;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float zz[C::S], ss[C::S];
+  for (int s = 0; s < C::S; ++s) vload(v[s], b + 4 * s);
+}
+template <class C>
+__device__ __forceinline__ void slab_store(float* slab, int pt, int kq, const float (&v)[C::S][4]) {
+  float* b = slab + kq * 512 + C::row0(pt) * 4;
 #pragma unroll
-    for (int k = 0; k < C::S; ++k) zz[k] = z[k][j];
-    tc_act1<C, ACT>(zz, ss);
+  for (int s = 0; s < C::S; ++s) vstore(b + 4 * s, v[s]);
+}
+template <class C>
+__device__ __forceinline__ void col(const float (&v)[C::S][4], int j, float (&o)[C::S]) {
 #pragma unroll
-    for (int k = 0; k < C::S; ++k) s[k][j] = ss[k];
+  for (int s = 0; s < C::S; ++s) o[s] = v[s][j];
+}
+
+__device__ __forceinline__ size_t tc_toff(const WArgs& a, int l, long long tile) {
+  return (size_t(l) * a.ntiles + tile) * size_t(a.WP) * 128;
+}
+
+// row-quad-major copy of a [4 kq][128][4] slab (units k0..k0+15) into a tile's
+// [32 rq][WP][4] buffer (128 threads).  Lane = (row quad, unit): it gathers
+// its unit's 4 rows with scalar shared loads and writes one 16-byte store, so
+// 16 lanes cover a contiguous 256-byte run.  Pad rows are written as zeros so
+// they contribute nothing to the weight gradients.
+template <class C>
+__device__ __forceinline__ void slab_store_t(const float* slab, float* dstT, int WP, int k0, int tid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int item = it * 128 + tid;
+    const int rq = item >> 4, k16 = item & 15;
+    const float* src = slab + (k16 >> 2) * 512 + (4 * rq) * 4 + (k16 & 3);
+    float v[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const float x = src[rr * 4];
+      v[rr] = ((4 * rq + rr) & 31) < C::VR ? x : 0.f;
+    }
+    *reinterpret_cast<float4*>(dstT + (size_t(rq) * WP + k0 + k16) * 4) = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
-template <class C, int ACT>
-__device__ __forceinline__ void tc_act_bwd4(const float (&z)[C::S][4], float (&sb)[C::S][4]) {
+// plain copy of a [4 kq][128][4] slab to its (contiguous 8 KB) place in HBM
+__device__ __forceinline__ void slab_copy_out(const float* slab, float* dst, int tid) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float zz[C::S], bb[C::S];
-#pragma unroll
-    for (int k = 0; k < C::S; ++k) {
-      zz[k] = z[k][j];
-      bb[k] = sb[k][j];
-    }
-    tc_act_bwd1<C, ACT>(zz, bb);
-#pragma unroll
-    for (int k = 0; k < C::S; ++k) sb[k][j] = bb[k];
-  }
+  for (int i = 0; i < 4; ++i)
+    reinterpret_cast<float4*>(dst)[tid + 128 * i] = reinterpret_cast<const float4*>(slab)[tid + 128 * i];
 }
 
 // TMEM allocation + mbarrier init (CTA-wide; every thread calls)
@@ -187,71 +220,92 @@ __device__ __forceinline__ void tc_teardown(uint32_t tmem) {
   if (threadIdx.x < 32) tc::tmem_free<NCOLS>(tmem);
 }
 
-// stage rows n0..n0+NB-1, columns [k0, k0+32) of a row-major matrix (row
-// length ld) as a K-major operand B[kq][NB][4]
-__device__ __forceinline__ void tc_stage_b(float* B, const float* __restrict__ M, int ld, int n0, int k0, int NB,
-                                           int tid, int nt) {
-  for (int i = tid; i < NB * 8; i += nt) {
-    const int nlo = i & 7, kq = (i >> 3) & 7, n = (i >> 6) * 8 + nlo;
-    cp_async16(B + (kq * NB + n) * 4, M + size_t(n0 + n) * ld + k0 + 4 * kq);
-  }
-}
-
-// issue the 4 K-steps of one 32-deep chunk (A[kq][MA][4], B[kq][NB][4])
-__device__ __forceinline__ void tc_mma_chunk(uint32_t tmem, const float* A, int MA, const float* B, int NB,
-                                             uint32_t idesc, bool first) {
+// 2 K-steps (16 deep) of A[kq][MA][4] x B[kq][NB][4]
+__device__ __forceinline__ void tc_mma16(uint32_t tmem, const float* A, int MA, const float* B, int NB, uint32_t idesc,
+                                         bool first) {
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk)
+  for (int kk = 0; kk < 2; ++kk)
     tc::mma_tf32(tmem, tc::desc(A + kk * 8 * MA, MA * 16, 128), tc::desc(B + kk * 8 * NB, NB * 16, 128), idesc,
                  (!first || kk) ? 1u : 0u);
 }
 
+// weight operand slab of chunk c (16 K values x NB units, contiguous NB*64 B)
+__device__ __forceinline__ const float* tc_wslab(const WArgs& a, long long base, int l, int nb, int c) {
+  const int nnb = a.WP / a.nb, nch = a.WP / TC_KC;
+  return static_cast<const float*>(a.kp) + base + ((size_t(l - 1) * nnb + nb) * nch + c) * size_t(a.nb) * 16;
+}
+
 // ---------------------------------------------------------------------------
 // forward, hidden layer l >= 1: Z_l = sigma(Z_{l-1}) W_l + b_l
-// grid (tiles, WP/NB), 128 threads
+// grid (tiles, WP/NB), 128 threads.  Ring stage = Z_{l-1} slab (8 KB, activated
+// in place) + W_l^T slab (NB x 16).
 // ---------------------------------------------------------------------------
 template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_fwd_kernel(WArgs a, int l, int NB) {
+__global__ void __launch_bounds__(128) tcw_fwd_kernel(WArgs a, int l) {
   using C = TcCfg<ACT, MODE, REG>;
   extern __shared__ __align__(128) unsigned char tc_smem[];
-  float* Ab = reinterpret_cast<float*>(tc_smem);  // [2][8][128][4]
-  float* Bb = Ab + 2 * C::NQ * 512;                // [2][8][NB][4]
-  __shared__ __align__(8) uint64_t mbar[2];
+  float* ring = reinterpret_cast<float*>(tc_smem);
+  __shared__ __align__(8) uint64_t full[TC_NS], empty[TC_NS];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long tile = blockIdx.x;
-  const int n0 = blockIdx.y * NB;
+  const int nb = blockIdx.y, NB = a.nb, n0 = nb * NB;
   const float* kp = static_cast<const float*>(a.kp);
   const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
-  const uint32_t tmem = tc_setup<256>(&tslot, mbar, 2);
-  const int nch = a.WP / C::KC;
+  if (tid == 0)
+    for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
+  const uint32_t tmem = tc_setup<256>(&tslot, empty, TC_NS);
+  const int nch = a.WP / TC_KC;
+  const bool virt = (l == 1);
+  const size_t SF = C::stage_floats(NB);
+  const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, 0));
+  auto produce = [&](int c) {
+    const int s = c % TC_NS;
+    float* st = ring + s * SF;
+    tc::mbar_expect_tx(&full[s], NB * 64 + (virt ? 0 : 8192));
+    tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
+    if (!virt) tc::bulk_g2s(st, zsrc + size_t(c) * 2048, 8192, &full[s]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < TC_NS && c < nch; ++c) produce(c);
   const uint32_t idesc = tc::idesc_tf32(128, NB);
   for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c >= 2) tc::mbar_wait(&mbar[b], ((c - 2) >> 1) & 1);
-    float* A = Ab + b * C::NQ * 512;
-    float* B = Bb + b * C::NQ * NB * 4;
-    tc_stage_b(B, kp + pl.off_wt(l), a.WP, n0, c * C::KC, NB, tid, C::NT);
-    cp_async_commit();
-    for (int i = tid; i < C::PPT * C::NQ; i += C::NT) {
+    const int s = c % TC_NS;
+    float* A = ring + s * SF;
+    tc::mbar_wait(&full[s], (c / TC_NS) & 1);
+    for (int i = tid; i < C::ITEMS; i += C::NT) {
       const int pt = i % C::PPT, kq = i / C::PPT;
-      float z[C::S][4], s[C::S][4];
-      tc_load_z<C>(a, kp, pl, l - 1, tile, pt, c * C::NQ + kq, z);
-      tc_act4<C, ACT>(z, s);
-      float* d = A + kq * 512 + C::row0(pt) * 4;
+      float z[C::S][4], sv[C::S][4];
+      if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, 4 * c + kq, z);
+      else slab_load<C>(z, A, pt, kq);
 #pragma unroll
-      for (int st = 0; st < C::S; ++st) vstore(d + 4 * st, s[st]);
+      for (int j = 0; j < 4; ++j) {
+        float zz[C::S], ss[C::S];
+        col<C>(z, j, zz);
+        tc_act1<C, ACT>(zz, ss);
+#pragma unroll
+        for (int k = 0; k < C::S; ++k) sv[k][j] = ss[k];
+      }
+      slab_store<C>(A, pt, kq, sv);
     }
-    cp_async_wait_all();
     tc::fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
-      tc_mma_chunk(tmem, A, 128, B, NB, idesc, c == 0);
-      tc::mma_commit(&mbar[b]);
+      tc_mma16(tmem, A, 128, A + 2048, NB, idesc, c == 0);
+      tc::mma_commit(&empty[s]);
+      // refill the stage of the previous chunk once its MMAs have drained
+      if (c >= 1 && c - 1 + TC_NS < nch) {
+        tc::mbar_wait(&empty[(c - 1) % TC_NS], ((c - 1) / TC_NS) & 1);
+        produce(c - 1 + TC_NS);
+      }
     }
+    // S_{l-1} row-quad major for the weight gradient (the N block 0 CTA writes it)
+#ifndef FR_NO_ST
+    if (nb == 0) slab_store_t<C>(A, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, tid);
+#endif
   }
-  tc::mbar_wait(&mbar[(nch - 1) & 1], ((nch - 1) >> 1) & 1);
+  tc::mbar_wait(&empty[(nch - 1) % TC_NS], ((nch - 1) / TC_NS) & 1);
   tc::fence_after();
   const int r = warp * 32 + lane;
   const bool vrow = lane < C::VR && (lane % C::S) == 0;
@@ -273,71 +327,143 @@ __global__ void __launch_bounds__(128) tcw_fwd_kernel(WArgs a, int l, int NB) {
 
 // ---------------------------------------------------------------------------
 // adjoint, hidden layer l >= 1: Zbar_{l-1} = act_bwd(Z_{l-1}, Zbar_l W_l^T)
-// grid (tiles, WP/NB), 128 threads
+// grid (tiles, WP/NB), 128 threads.  Main loop: one thread streams Zbar_l and
+// W_l slabs and issues the MMAs.  Epilogue (16 columns at a time): TMEM ->
+// shared S-bar slab, Z_{l-1} slab prefetched by bulk copy, point-major act-bwd.
+// For l == 1 the layer-0 adjoint is reduced straight into per-tile dW_0 | db_0
+// partials (Zbar_0 is never stored).
 // ---------------------------------------------------------------------------
 template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l, int NB) {
+__global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l) {
   using C = TcCfg<ACT, MODE, REG>;
+  constexpr int DIN = C::DIN, D1 = DIN + 1;
   extern __shared__ __align__(128) unsigned char tc_smem[];
-  float* Ab = reinterpret_cast<float*>(tc_smem);
-  float* Bb = Ab + 2 * C::NQ * 512;
-  __shared__ __align__(8) uint64_t mbar[2];
+  float* ring = reinterpret_cast<float*>(tc_smem);
+  __shared__ __align__(8) uint64_t full[TC_NS], empty[TC_NS], zfull[2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long tile = blockIdx.x;
-  const int n0 = blockIdx.y * NB;
+  const int nb = blockIdx.y, NB = a.nb, n0 = nb * NB;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
-  const uint32_t tmem = tc_setup<256>(&tslot, mbar, 2);
-  const int nch = a.WP / C::KC;
-  const uint32_t idesc = tc::idesc_tf32(128, NB);
+  const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
+  if (tid == 0) {
+    for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
+    tc::mbar_init(&zfull[0], 1);
+    tc::mbar_init(&zfull[1], 1);
+  }
+  const uint32_t tmem = tc_setup<256>(&tslot, empty, TC_NS);
+  const int nch = a.WP / TC_KC;
+  const size_t SF = C::stage_floats(NB);
   const float* zb = static_cast<const float*>(a.adj) + tc_off(a, l, tile, 0);
-  for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c >= 2) tc::mbar_wait(&mbar[b], ((c - 2) >> 1) & 1);
-    float* A = Ab + b * C::NQ * 512;
-    float* B = Bb + b * C::NQ * NB * 4;
-    tc_stage_b(B, kp + pl.off_w(l), a.WP, n0, c * C::KC, NB, tid, C::NT);
-    const float* src = zb + size_t(c) * C::NQ * 512;
-    for (int i = tid; i < C::NQ * 128; i += C::NT) cp_async16(A + 4 * i, src + 4 * i);
-    cp_async_commit();
-    cp_async_wait_all();
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
+  if (tid == 0) {
+    auto produce = [&](int c) {
+      const int s = c % TC_NS;
+      float* st = ring + s * SF;
+      tc::mbar_expect_tx(&full[s], NB * 64 + 8192);
+      tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_d, l, nb, c), NB * 64, &full[s]);
+      tc::bulk_g2s(st, zb + size_t(c) * 2048, 8192, &full[s]);
+    };
+    for (int c = 0; c < TC_NS && c < nch; ++c) produce(c);
+    const uint32_t idesc = tc::idesc_tf32(128, NB);
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % TC_NS;
+      float* st = ring + s * SF;
+      tc::mbar_wait(&full[s], (c / TC_NS) & 1);
       tc::fence_after();
-      tc_mma_chunk(tmem, A, 128, B, NB, idesc, c == 0);
-      tc::mma_commit(&mbar[b]);
+      tc_mma16(tmem, st, 128, st + 2048, NB, idesc, c == 0);
+      tc::mma_commit(&empty[s]);
+      if (c >= 1 && c - 1 + TC_NS < nch) {
+        tc::mbar_wait(&empty[(c - 1) % TC_NS], ((c - 1) / TC_NS) & 1);
+        produce(c - 1 + TC_NS);
+      }
     }
   }
-  tc::mbar_wait(&mbar[(nch - 1) & 1], ((nch - 1) >> 1) & 1);
+  tc::mbar_wait(&empty[(nch - 1) % TC_NS], ((nch - 1) / TC_NS) & 1);
   tc::fence_after();
-  // S-bar columns in chunks of 32 through shared memory (point-major act-bwd)
-  float* stg = Ab;  // [8][128][4]
+  __syncthreads();  // every thread is past the ring before it is reused
+  // epilogue buffers inside the (now idle) ring
+  float* stg = ring;             // [4][128][4]  S-bar columns
+  float* zc = ring + 2048;       // [2][4][128][4] Z_{l-1} slabs
+  float* red = ring + 3 * 2048;  // [PPT][4 kq][4 j][D1] dW_0 contributions
+  const bool virt = (l == 1);
+  const int nck = NB / 16;
+  const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, n0 / 4));
+  if (!virt && tid == 0)
+    for (int j = 0; j < 2 && j < nck; ++j) {
+      tc::mbar_expect_tx(&zfull[j], 8192);
+      tc::bulk_g2s(zc + j * 2048, zsrc + size_t(j) * 2048, 8192, &zfull[j]);
+    }
   const int r = warp * 32 + lane;
-  for (int c0 = 0; c0 < NB; c0 += 32) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
+  const float* pts = static_cast<const float*>(a.pts);
+  for (int j = 0; j < nck; ++j) {
+    {
       float v[16];
-      tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0 + 16 * h, v);
+      tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16 * j, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float4*>(stg + (4 * h + q) * 512 + r * 4) =
-            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        *reinterpret_cast<float4*>(stg + q * 512 + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     __syncthreads();
-    for (int i = tid; i < C::PPT * C::NQ; i += C::NT) {
+    if (!virt) tc::mbar_wait(&zfull[j & 1], (j >> 1) & 1);
+    const float* zs = zc + (j & 1) * 2048;
+    for (int i = tid; i < C::ITEMS; i += C::NT) {
       const int pt = i % C::PPT, kq = i / C::PPT;
-      const int q = (n0 + c0) / 4 + kq;
+      const int q = n0 / 4 + 4 * j + kq;
       float z[C::S][4], sb[C::S][4];
-      tc_load_z<C>(a, kp, pl, l - 1, tile, pt, q, z);
-      const float* sp = stg + kq * 512 + C::row0(pt) * 4;
+      if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
+      else slab_load<C>(z, zs, pt, kq);
+      slab_load<C>(sb, stg, pt, kq);
 #pragma unroll
-      for (int st = 0; st < C::S; ++st) vload(sb[st], sp + 4 * st);
-      tc_act_bwd4<C, ACT>(z, sb);
-      float* d = static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, q) + C::row0(pt) * 4;
+      for (int jj = 0; jj < 4; ++jj) {
+        float zz[C::S], bb[C::S], sa[C::S];
+        col<C>(z, jj, zz);
+        col<C>(sb, jj, bb);
+        tc_act_bwd1<C, ACT>(zz, bb, sa);
 #pragma unroll
-      for (int st = 0; st < C::S; ++st) vstore(d + 4 * st, sb[st]);
+        for (int k = 0; k < C::S; ++k) sb[k][jj] = bb[k];
+      }
+      if (!virt) {
+        slab_store<C>(stg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
+      } else {
+        // dW_0[i][u] += x_i zbar_v + zbar_{g_i} ; db_0[u] += zbar_v (zero for padding points)
+        const long long p = tile * C::PPT + pt;
+        const bool live = p < a.n;
+        float x[DIN];
+#pragma unroll
+        for (int ii = 0; ii < DIN; ++ii) x[ii] = live ? pts[p * DIN + ii] : 0.f;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+          const float zv = live ? sb[0][jj] : 0.f;
+#pragma unroll
+          for (int ii = 0; ii < DIN; ++ii) {
+            float t = x[ii] * zv;
+            if constexpr (C::JET) t += live ? sb[1 + ii][jj] : 0.f;
+            rd[ii] = t;
+          }
+          rd[DIN] = zv;
+        }
+      }
+    }
+    __syncthreads();
+    if (!virt) {
+      if (tid == 0 && j + 2 < nck) {
+        tc::mbar_expect_tx(&zfull[j & 1], 8192);
+        tc::bulk_g2s(zc + (j & 1) * 2048, zsrc + size_t(j + 2) * 2048, 8192, &zfull[j & 1]);
+      }
+      slab_copy_out(stg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), tid);
+#ifndef FR_NO_ST
+      slab_store_t<C>(stg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, tid);
+#endif
+    } else {
+      // fixed-order sum over the tile's points -> p0[tile][i*WP + u] (i == DIN: db_0)
+      for (int e = tid; e < 16 * D1; e += C::NT) {
+        const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
+        float acc = 0.f;
+        for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + jj) * D1 + ii];
+        const int u = n0 + 16 * j + 4 * kq + jj;
+        a.p0[size_t(tile) * (D1 * a.WP) + size_t(ii) * a.WP + u] = acc;
+      }
     }
     __syncthreads();
   }
@@ -345,202 +471,202 @@ __global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l, int NB) {
 }
 
 // ---------------------------------------------------------------------------
-// dW_l = sum_rows sigma(Z_{l-1})^T Zbar_l, db_l = sum of value rows of Zbar_l.
-// grid (ceil(WP/128) k-blocks, WP/NB u-blocks, KS row splits), 256 threads.
-// Per 32-row group: threads 0..127 (one per input unit k) apply the jet
-// activation point by point and write their column K-major ([row quad][k][4]);
-// threads 128..255 transpose Zbar 4x4 blocks into [row quad][u][4].
+// dW_l = sum_rows S_{l-1}^T Zbar_l (+ db_l = sum of value rows of Zbar_l).
+// Both operands arrive row-quad major (written by the forward / adjoint
+// kernels), i.e. already K-major for K = rows, so this is a pure stream:
+//   warp 0     loader: per 32-row group, one bulk copy of S_{l-1} (all WP
+//              units, WP*128 B) + the Zbar_l N block (NB*128 B) into an
+//              NS-stage ring;
+//   warp 1     MMA issuer: nkb = ceil(WP/128) accumulators of 128 x NB in
+//              TMEM (nkb * NB <= 512 columns), 4 K-steps per group;
+//   warps 2-9  db_l (one unit per thread) and the final TMEM -> HBM drain.
+// grid (WP/NB, splits), one CTA per SM.
 // ---------------------------------------------------------------------------
+constexpr int TC_DW_MAXNS = 4;
 template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(256) tcw_dw_kernel(WArgs a, int l, int NB) {
+__global__ void __launch_bounds__(320) tcw_dw_kernel(WArgs a, int l, int NB, int NS) {
   using C = TcCfg<ACT, MODE, REG>;
-  constexpr int S = C::S, ZRS = C::ZRS;
+  constexpr int S = C::S;
   extern __shared__ __align__(128) unsigned char tc_smem[];
-  float* As = reinterpret_cast<float*>(tc_smem);  // [2][8][128][4]
-  float* Bs = As + 2 * 8 * 512;                    // [2][8][NB][4]
-  float* Zs = Bs + 2 * 8 * NB * 4;                 // [32 quads][ZRS]
-  __shared__ __align__(8) uint64_t mbar[2];
+  const int WP = a.WP;
+  const int SF = (WP + NB) * 32;  // stage floats: A [8][WP][4] then B [8][NB][4]
+  float* ring = reinterpret_cast<float*>(tc_smem);
+  __shared__ __align__(8) uint64_t full[TC_DW_MAXNS], empty[TC_DW_MAXNS], done;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kb = blockIdx.x, n0 = blockIdx.y * NB, split = blockIdx.z;
-  const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
-  const uint32_t tmem = tc_setup<256>(&tslot, mbar, 2);
-  const uint32_t idesc = tc::idesc_tf32(128, NB);
-  const int kq0 = kb * 32;                                   // first input-unit quad of this block
-  const int nkq = min(32, a.WP / 4 - kq0);                   // valid quads in the block
-  const int k = kb * 128 + tid;                              // A producer's input unit (tid < 128)
-  float db4[4] = {0.f, 0.f, 0.f, 0.f};
-  int ci = 0;
-  for (long long t = split; t < a.ntiles; t += gridDim.z) {
-    for (int g = 0; g < 4; ++g, ++ci) {
-      const int b = ci & 1;
-      if (ci >= 2) tc::mbar_wait(&mbar[b], ((ci - 2) >> 1) & 1);
-      float* A = As + b * 8 * 512;
-      float* B = Bs + b * 8 * NB * 4;
-      if (l - 1 >= 1) {
-        const float* zsrc = static_cast<const float*>(a.act) + tc_off(a, l - 1, t, kq0) + g * 128;
-        for (int i = tid; i < nkq * 32; i += C::DW_NT) {
-          const int kq = i >> 5, rr = i & 31;
-          cp_async16(Zs + kq * ZRS + rr * 4, zsrc + size_t(kq) * 512 + rr * 4);
-        }
-        cp_async_commit();
-      }
-      if (tid >= 128) {
-        // Zbar rows g*32.. of this tile, unit quads n0/4 .. +NB/4: 4x4 transposes
-        const float* zb = static_cast<const float*>(a.adj) + tc_off(a, l, t, n0 / 4) + g * 128;
-        for (int i = tid - 128; i < (NB / 4) * 8; i += 128) {
-          const int uq = i % (NB / 4), rq = i / (NB / 4);
-          float m[4][4];
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const int row = 4 * rq + rr;
-            if (row < C::VR) {
-              vload(m[rr], zb + size_t(uq) * 512 + row * 4);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) m[rr][j] = 0.f;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float4*>(B + (rq * NB + 4 * uq + j) * 4) = make_float4(m[0][j], m[1][j], m[2][j], m[3][j]);
-        }
-        // db_l: one fixed unit quad per thread, value rows in point order
-        if (kb == 0 && tid - 128 < NB / 4)
-          for (int pp = 0; pp < C::PPW; ++pp) {
-            float v[4];
-            vload(v, zb + size_t(tid - 128) * 512 + pp * S * 4);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) db4[j] += v[j];
-          }
-      }
-      if (l - 1 >= 1) cp_async_wait_all();
-      __syncthreads();
-      if (tid < 128) {
-        float col[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) col[i] = 0.f;
-        if (k < a.WP) {
-#pragma unroll
-          for (int pp = 0; pp < C::PPW; ++pp) {
-            float z[S], s[S];
-            if (l - 1 >= 1) {
-#pragma unroll
-              for (int st = 0; st < S; ++st) z[st] = Zs[(tid >> 2) * ZRS + (pp * S + st) * 4 + (tid & 3)];
-            } else {
-              const long long p = t * C::PPT + g * C::PPW + pp;
-              const float* pts = static_cast<const float*>(a.pts);
-              float zv = 0.f;
-#pragma unroll
-              for (int i = 0; i < C::DIN; ++i) zv = fmaf(p < a.n ? pts[p * C::DIN + i] : 0.f, kp[pl.off_w(0) + i * a.WP + k], zv);
-              z[0] = zv + kp[pl.off_b(0) + k];
-              if constexpr (C::JET) {
-#pragma unroll
-                for (int i = 0; i < C::NG; ++i) z[1 + i] = kp[pl.off_w(0) + i * a.WP + k];
-#pragma unroll
-                for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i] = 0.f;
-              }
-            }
-            tc_act1<C, ACT>(z, s);
-#pragma unroll
-            for (int st = 0; st < S; ++st) col[pp * S + st] = s[st];
-          }
-        }
-#pragma unroll
-        for (int rq = 0; rq < 8; ++rq)
-          *reinterpret_cast<float4*>(A + (rq * 128 + tid) * 4) =
-              make_float4(col[4 * rq], col[4 * rq + 1], col[4 * rq + 2], col[4 * rq + 3]);
-      }
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after();
-        tc_mma_chunk(tmem, A, 128, B, NB, idesc, ci == 0);
-        tc::mma_commit(&mbar[b]);
-      }
+  const int nbk = blockIdx.x, n0 = nbk * NB, split = blockIdx.y;
+  const int nkb = (WP + 127) / 128;
+  const ParamLayout pl{C::DIN, WP, C::NOUT, a.L};
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1 + 8);  // MMA commit + the 8 db warps
     }
+    tc::mbar_init(&done, 1);
   }
+  const uint32_t tmem = tc_setup<512>(&tslot, nullptr, 0);
+  const long long my_tiles = split < a.ntiles ? (a.ntiles - 1 - split) / gridDim.y + 1 : 0;
+  const long long nchunks = 4 * my_tiles;
   double* gp = a.gpart + size_t(split) * a.np_pad;
-  if (kb == 0 && ci > 0 && tid >= 128 && tid - 128 < NB / 4)
+  if (warp == 0) {
+    if (lane == 0)
+      for (long long ci = 0; ci < nchunks; ++ci) {
+        const int s = int(ci % NS);
+        const long long t = split + (ci >> 2) * gridDim.y;
+        const int g = int(ci & 3);
+        if (ci >= NS) tc::mbar_wait(&empty[s], ((ci - NS) / NS) & 1);
+        float* A = ring + s * SF;
+        float* B = A + WP * 32;
+        tc::mbar_expect_tx(&full[s], uint32_t(WP + NB) * 128);
+        tc::bulk_g2s(A, a.st + tc_toff(a, l - 1, t) + size_t(g) * 8 * WP * 4, WP * 128, &full[s]);
+        const float* zsrc = a.zt + tc_toff(a, l, t) + (size_t(g) * 8 * WP + n0) * 4;
+        if (NB == WP) {
+          tc::bulk_g2s(B, zsrc, NB * 128, &full[s]);
+        } else {
+          for (int rq = 0; rq < 8; ++rq) tc::bulk_g2s(B + rq * NB * 4, zsrc + size_t(rq) * WP * 4, NB * 16, &full[s]);
+        }
+      }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, NB);
+      for (long long ci = 0; ci < nchunks; ++ci) {
+        const int s = int(ci % NS);
+        tc::mbar_wait(&full[s], (ci / NS) & 1);
+        tc::fence_after();
+        const float* A = ring + s * SF;
+        const float* B = A + WP * 32;
+        for (int kb = 0; kb < nkb; ++kb)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) gp[pl.off_b(l) + n0 + 4 * (tid - 128) + j] = double(db4[j]);
-  if (ci > 0) {
-    tc::mbar_wait(&mbar[(ci - 1) & 1], ((ci - 1) >> 1) & 1);
-    tc::fence_after();
-    // warps w and w+4 share TMEM lane quadrant w: column halves
-    const int quad = warp & 3, half = warp >> 2;
-    const int kr = kb * 128 + quad * 32 + lane;
-    for (int c0 = half * 16; c0 < NB; c0 += 32) {
-      float v[16];
-      tc::tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + c0, v);
-      if (kr < a.WP) {
-        double* dst = gp + pl.off_w(l) + size_t(kr) * a.WP + n0 + c0;
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_tf32(tmem + kb * NB, tc::desc(A + kb * 512 + kk * 8 * WP, WP * 16, 128),
+                         tc::desc(B + kk * 8 * NB, NB * 16, 128), idesc, (ci || kk) ? 1u : 0u);
+        tc::mma_commit(&empty[s]);
+      }
+      if (nchunks > 0) tc::mma_commit(&done);
+    }
+  } else {
+    // ---- db_l (unit u per thread) ----
+    const int u = tid - 64;  // 0..255
+    float db = 0.f;
+    for (long long ci = 0; ci < nchunks; ++ci) {
+      const int s = int(ci % NS);
+      tc::mbar_wait(&full[s], (ci / NS) & 1);
+      if (u < NB) {
+        const float* B = ring + s * SF + WP * 32;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dst[i] = double(v[i]);
+        for (int pp = 0; pp < C::PPW; ++pp) {
+          const int r = pp * S;
+          db += B[((r >> 2) * NB + u) * 4 + (r & 3)];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&empty[s])) : "memory");
+    }
+    if (nchunks > 0) {
+      if (u < NB) gp[pl.off_b(l) + n0 + u] = double(db);
+      tc::mbar_wait(&done, 0);
+      tc::fence_after();
+      // warps 2..9: TMEM lane quadrant warp % 4, column half (warp - 2) / 4
+      const int quad = warp & 3, half = (warp - 2) >> 2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int kr = kb * 128 + quad * 32 + lane;
+        for (int c0 = half * 16; c0 < NB; c0 += 32) {
+          float v[16];
+          tc::tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + kb * NB + c0, v);
+          if (kr < WP) {
+            double* dst = gp + pl.off_w(l) + size_t(kr) * WP + n0 + c0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dst[i] = double(v[i]);
+          }
+        }
       }
     }
   }
-  tc_teardown<256>(tmem);
+  tc_teardown<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------
-// head: output layer + residual / MSE + Ybar + S-bar_{L-1} + act-bwd -> Zbar_{L-1}
-// grid tiles, 128 threads: QS threads per point split the WP/4 unit quads
+// head: output layer + residual / MSE + Ybar + S-bar_{L-1} + act-bwd -> Zbar_{L-1},
+// with the per-tile dW_L | db_L partials.  grid tiles, 128 threads; Z_{L-1} is
+// streamed twice through a bulk-copy ring (forward pass, then adjoint pass).
 // ---------------------------------------------------------------------------
 template <int ACT, int MODE, int REG>
 __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   using C = TcCfg<ACT, MODE, REG>;
-  constexpr int NT = C::NT, PPT = C::PPT, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S, QS = C::QS;
+  constexpr int NT = C::NT, PPT = C::PPT, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
   constexpr int NG = C::NG, LAP0 = C::LAP0, SN = S * NOUT;
   extern __shared__ __align__(128) unsigned char tc_smem[];
-  double* red = reinterpret_cast<double*>(tc_smem);  // [2][NT]
-  float* WLs = reinterpret_cast<float*>(red + 2 * NT);  // [WP][NOUT]
-  float* Yp = WLs + a.WP * NOUT;                        // [PPT*QS][SN]
-  float* Ys = Yp + PPT * QS * SN;                       // [PPT][SN]
-  float* Ybs = Ys + PPT * SN;                           // [PPT][SN]
+  double* lred = reinterpret_cast<double*>(tc_smem);      // [2][NT]
+  float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][2048]
+  float* WLs = ring + TC_NS * 2048;                        // [WP][NOUT]
+  float* Yp = WLs + a.WP * NOUT;                           // [NT][SN]
+  float* Ys = Yp + NT * SN;                                // [PPT][SN]
+  float* Ybs = Ys + PPT * SN;                              // [PPT][SN]
+  float* red = Ybs + PPT * SN;                             // [PPT][4][4][NOUT]
+  __shared__ __align__(8) uint64_t full[TC_NS];
   const long long tile = blockIdx.x;
-  const int tid = threadIdx.x, pt = tid / QS, qs = tid % QS;
-  const bool active = tid < PPT * QS;
+  const int tid = threadIdx.x;
   const float* kp = static_cast<const float*>(a.kp);
   const ParamLayout pl{C::DIN, a.WP, NOUT, a.L};
-  const int L = a.L, NQW = a.WP / 4;
+  const int L = a.L, nch = a.WP / TC_KC, ntot = 2 * nch;
+  const float* zsrc = static_cast<const float*>(a.act) + tc_off(a, L - 1, tile, 0);
+  if (tid == 0) {
+    for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  auto produce = [&](int g) {
+    const int s = g % TC_NS;
+    tc::mbar_expect_tx(&full[s], 8192);
+    tc::bulk_g2s(ring + s * 2048, zsrc + size_t(g % nch) * 2048, 8192, &full[s]);
+  };
+  if (tid == 0)
+    for (int g = 0; g < TC_NS && g < ntot; ++g) produce(g);
   for (int i = tid; i < a.WP * NOUT; i += NT) WLs[i] = kp[pl.off_w(L) + i];
   __syncthreads();
-  if (active) {
-    float y[S][NOUT];
+  // ---- forward: Y partials per (point, kq) thread ----
+  float y[S][NOUT];
 #pragma unroll
-    for (int st = 0; st < S; ++st)
+  for (int st = 0; st < S; ++st)
 #pragma unroll
-      for (int c = 0; c < NOUT; ++c) y[st][c] = 0.f;
-    for (int q = qs; q < NQW; q += QS) {
-      float z[S][4], s[S][4];
-      tc_load_z<C>(a, kp, pl, L - 1, tile, pt, q, z);
-      tc_act4<C, ACT>(z, s);
+    for (int o = 0; o < NOUT; ++o) y[st][o] = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % TC_NS;
+    tc::mbar_wait(&full[s], (c / TC_NS) & 1);
+    for (int i = tid; i < C::ITEMS; i += NT) {
+      const int pt = i % PPT, kq = i / PPT;
+      float z[S][4];
+      slab_load<C>(z, ring + s * 2048, pt, kq);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j) {
+        float zz[S], ss[S];
+        col<C>(z, j, zz);
+        tc_act1<C, ACT>(zz, ss);
+        const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
 #pragma unroll
-        for (int c = 0; c < NOUT; ++c) {
-          const float w = WLs[(4 * q + j) * NOUT + c];
+        for (int st = 0; st < S; ++st)
 #pragma unroll
-          for (int st = 0; st < S; ++st) y[st][c] = fmaf(s[st][j], w, y[st][c]);
-        }
+          for (int o = 0; o < NOUT; ++o) y[st][o] = fmaf(ss[st], w[o], y[st][o]);
+      }
     }
-#pragma unroll
-    for (int st = 0; st < S; ++st)
-#pragma unroll
-      for (int c = 0; c < NOUT; ++c) Yp[tid * SN + st * NOUT + c] = y[st][c];
+    __syncthreads();
+    if (tid == 0 && c + TC_NS < ntot) produce(c + TC_NS);
   }
+#pragma unroll
+  for (int st = 0; st < S; ++st)
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) Yp[tid * SN + st * NOUT + o] = y[st][o];
   __syncthreads();
   const long long p0 = tile * PPT, rem = a.n - p0;
   double lacc0 = 0.0, lacc1 = 0.0;
-  if (active && qs == 0) {
-    float* y = Ys + pt * SN;
+  if (tid < PPT) {
+    const int pt = tid;
+    float* yv = Ys + pt * SN;
     float* yb = Ybs + pt * SN;
     for (int i = 0; i < SN; ++i) {
       float v = 0.f;
-      for (int h = 0; h < QS; ++h) v += Yp[(pt * QS + h) * SN + i];
-      y[i] = (i < NOUT) ? v + kp[pl.off_b(L) + i] : v;
+      for (int h = 0; h < C::TPP; ++h) v += Yp[(pt + PPT * h) * SN + i];
+      yv[i] = (i < NOUT) ? v + kp[pl.off_b(L) + i] : v;
       yb[i] = 0.f;
     }
     if (pt < rem) {
@@ -548,10 +674,10 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
         using Rg = Regime<REG>;
         constexpr int NSP = Rg::NSP, TOFF = Rg::HAS_T, P = NVEL;
         const float inv_re = float(a.inv_re), two_coef = float(2.0 * a.coef);
-        auto Y = [&](int s, int c) { return y[s * NOUT + c]; };
+        auto Y = [&](int s, int o) { return yv[s * NOUT + o]; };
         auto GRAD = [&](int in) { return 1 + in; };
         auto LAP = [&](int in) { return 1 + NG + (in - LAP0); };
-        float r[NVEL + 1];
+        float rr[NVEL + 1];
 #pragma unroll
         for (int i = 0; i < NVEL; ++i) {
           const int xi = TOFF + i;
@@ -562,19 +688,19 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
           for (int jj = 0; jj < NSP; ++jj) acc += -inv_re * Y(LAP(TOFF + jj), i);
 #pragma unroll
           for (int kk = 0; kk < NVEL; ++kk) acc += Y(0, kk) * Y(GRAD(TOFF + kk), i);
-          r[i] = acc;
+          rr[i] = acc;
         }
         {
           float acc = Y(GRAD(TOFF), 0);
 #pragma unroll
           for (int kk = 1; kk < NVEL; ++kk) acc += Y(GRAD(TOFF + kk), kk);
-          r[NVEL] = acc;
+          rr[NVEL] = acc;
         }
 #pragma unroll
-        for (int i = 0; i <= NVEL; ++i) lacc0 += double(r[i]) * double(r[i]);
+        for (int i = 0; i <= NVEL; ++i) lacc0 += double(rr[i]) * double(rr[i]);
 #pragma unroll
         for (int i = 0; i < NVEL; ++i) {
-          const float rb = two_coef * r[i];
+          const float rb = two_coef * rr[i];
           if constexpr (Rg::HAS_T) yb[GRAD(0) * NOUT + i] += rb;
           yb[GRAD(TOFF + i) * NOUT + P] += rb;
 #pragma unroll
@@ -585,168 +711,114 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
             yb[GRAD(TOFF + kk) * NOUT + i] += rb * Y(0, kk);
           }
         }
-        const float rb = two_coef * r[NVEL];
+        const float rb = two_coef * rr[NVEL];
 #pragma unroll
         for (int kk = 0; kk < NVEL; ++kk) yb[GRAD(TOFF + kk) * NOUT + kk] += rb;
       } else {  // MSE
         const float two_vc = float(2.0 * a.coef), two_pc = float(2.0 * a.pcoef);
         const float* tu = static_cast<const float*>(a.tu) + (p0 + pt) * NVEL;
 #pragma unroll
-        for (int c = 0; c < NVEL; ++c) {
-          const float d = y[c] - tu[c];
-          lacc0 += a.velw[c] * (double(d) * double(d));
-          yb[c] = (two_vc * float(a.velw[c])) * d;
+        for (int o = 0; o < NVEL; ++o) {
+          const float d = yv[o] - tu[o];
+          lacc0 += a.velw[o] * (double(d) * double(d));
+          yb[o] = (two_vc * float(a.velw[o])) * d;
         }
         if (a.has_p) {
-          const float d = y[NVEL] - static_cast<const float*>(a.tp)[p0 + pt];
+          const float d = yv[NVEL] - static_cast<const float*>(a.tp)[p0 + pt];
           lacc1 += double(d) * double(d);
           yb[NVEL] = two_pc * d;
         }
       }
     }
-    float* yout = static_cast<float*>(a.ybar) + (size_t(tile) * 128 + C::row0(pt)) * NOUT;
-    for (int i = 0; i < SN; ++i) yout[i] = yb[i];
   }
-  red[tid] = lacc0;
-  red[NT + tid] = lacc1;
+  lred[tid] = lacc0;
+  lred[NT + tid] = lacc1;
   __syncthreads();
+  const size_t plen = size_t(a.WP) * NOUT + NOUT;
+  float* pL = a.pL + size_t(tile) * plen;
   if (tid == 0) {
     double s0 = 0.0, s1 = 0.0;
     for (int i = 0; i < NT; ++i) {
-      s0 += red[i];
-      s1 += red[NT + i];
+      s0 += lred[i];
+      s1 += lred[NT + i];
     }
     a.lpart[2 * tile] = s0;
     a.lpart[2 * tile + 1] = s1;
   }
-  if (!active) return;
-  const float* yb = Ybs + pt * SN;
-  for (int q = qs; q < NQW; q += QS) {
-    float z[S][4], sb[S][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int st = 0; st < S; ++st) {
-        float v = 0.f;
-#pragma unroll
-        for (int c = 0; c < NOUT; ++c) v = fmaf(yb[st * NOUT + c], WLs[(4 * q + j) * NOUT + c], v);
-        sb[st][j] = v;
-      }
-    tc_load_z<C>(a, kp, pl, L - 1, tile, pt, q, z);
-    tc_act_bwd4<C, ACT>(z, sb);
-    float* d = static_cast<float*>(a.adj) + tc_off(a, L - 1, tile, q) + C::row0(pt) * 4;
-#pragma unroll
-    for (int st = 0; st < S; ++st) vstore(d + 4 * st, sb[st]);
+  if (tid < NOUT) {  // db_L: value-row adjoints summed in point order
+    float acc = 0.f;
+    for (int pt = 0; pt < PPT; ++pt) acc += Ybs[pt * SN + tid];
+    pL[size_t(a.WP) * NOUT + tid] = acc;
   }
-}
-
-// dW_L, db_L from sigma(Z_{L-1}) and Ybar; grid KS, one unit quad per thread
-template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_dwL_kernel(WArgs a) {
-  using C = TcCfg<ACT, MODE, REG>;
-  constexpr int NOUT = C::NOUT, S = C::S;
-  const int ks = blockIdx.x, tid = threadIdx.x;
-  const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, NOUT, a.L};
-  double* gp = a.gpart + size_t(ks) * a.np_pad;
-  const int q = tid;
-  const bool active = q < a.WP / 4;
-  float acc[4][NOUT], db[NOUT];
+  // ---- adjoint: S-bar = Ybar W_L^T, act-bwd, dW_L partial ----
+  for (int c = 0; c < nch; ++c) {
+    const int g = nch + c, s = g % TC_NS;
+    float* slab = ring + s * 2048;
+    tc::mbar_wait(&full[s], (g / TC_NS) & 1);
+    for (int i = tid; i < C::ITEMS; i += NT) {
+      const int pt = i % PPT, kq = i / PPT;
+      const int q = 4 * c + kq;
+      const float* yb = Ybs + pt * SN;
+      float z[S][4], sb[S][4];
+      slab_load<C>(z, slab, pt, kq);
 #pragma unroll
-  for (int c = 0; c < NOUT; ++c) {
-    db[c] = 0.f;
+      for (int j = 0; j < 4; ++j) {
+        const float* w = WLs + (4 * q + j) * NOUT;
+        float zz[S], bb[S], sa[S];
+        col<C>(z, j, zz);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j][c] = 0.f;
-  }
-  int since = 0;
-  auto flush = [&]() {
-    if (active)
+        for (int st = 0; st < S; ++st) {
+          float v = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int c = 0; c < NOUT; ++c) {
-          red_add(gp + pl.off_w(a.L) + (4 * q + j) * NOUT + c, double(acc[j][c]));
-          acc[j][c] = 0.f;
+          for (int o = 0; o < NOUT; ++o) v = fmaf(yb[st * NOUT + o], w[o], v);
+          bb[st] = v;
         }
-    if (tid == 0)
+        tc_act_bwd1<C, ACT>(zz, bb, sa);
 #pragma unroll
-      for (int c = 0; c < NOUT; ++c) {
-        red_add(gp + pl.off_b(a.L) + c, double(db[c]));
-        db[c] = 0.f;
+        for (int st = 0; st < S; ++st) sb[st][j] = bb[st];
+        float* rd = red + ((pt * 4 + kq) * 4 + j) * NOUT;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+          float v = 0.f;
+#pragma unroll
+          for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
+          rd[o] = v;
+        }
       }
-  };
-  for (long long t = ks; t < a.ntiles; t += gridDim.x) {
-    const float* ybt = static_cast<const float*>(a.ybar) + size_t(t) * 128 * NOUT;
-    if (active) {
-      for (int pt = 0; pt < C::PPT; ++pt) {
-        float z[S][4], s[S][4];
-        tc_load_z<C>(a, kp, pl, a.L - 1, t, pt, q, z);
-        tc_act4<C, ACT>(z, s);
-        const float* yb = ybt + C::row0(pt) * NOUT;
-#pragma unroll
-        for (int st = 0; st < S; ++st)
-#pragma unroll
-          for (int c = 0; c < NOUT; ++c) {
-            const float y = yb[st * NOUT + c];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j][c] = fmaf(s[st][j], y, acc[j][c]);
-          }
-      }
+      slab_store<C>(slab, pt, kq, sb);  // Zbar_{L-1} in place of Z_{L-1}
     }
-    if (tid == 0)
-      for (int pt = 0; pt < C::PPT; ++pt)
-#pragma unroll
-        for (int c = 0; c < NOUT; ++c) db[c] += ybt[C::row0(pt) * NOUT + c];
-    if (++since == 8) {
-      flush();
-      since = 0;
+    __syncthreads();
+    slab_copy_out(slab, static_cast<float*>(a.adj) + tc_off(a, L - 1, tile, 4 * c), tid);
+    slab_store_t<C>(slab, a.zt + tc_toff(a, L - 1, tile), a.WP, 16 * c, tid);
+    for (int e = tid; e < 16 * NOUT; e += NT) {
+      const int kq = e / (4 * NOUT), j = (e / NOUT) % 4, o = e % NOUT;
+      float acc = 0.f;
+      for (int pt = 0; pt < PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + j) * NOUT + o];
+      pL[size_t(16 * c + 4 * kq + j) * NOUT + o] = acc;
     }
+    __syncthreads();
+    if (tid == 0 && g + TC_NS < ntot) produce(g + TC_NS);
   }
-  if (since) flush();
 }
 
-// dW_0, db_0 from the points and Zbar_0; grid (KS, ceil(WP/128)), one unit per thread
-template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_dw0_kernel(WArgs a) {
-  using C = TcCfg<ACT, MODE, REG>;
-  constexpr int DIN = C::DIN;
-  const int ks = blockIdx.x, u = threadIdx.x + blockIdx.y * 128;
-  const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
-  double* gp = a.gpart + size_t(ks) * a.np_pad;
-  if (u >= a.WP) return;
-  float acc[DIN + 1];
-#pragma unroll
-  for (int j = 0; j <= DIN; ++j) acc[j] = 0.f;
-  int since = 0;
-  auto flush = [&]() {
-#pragma unroll
-    for (int j = 0; j < DIN; ++j) {
-      red_add(gp + pl.off_w(0) + j * a.WP + u, double(acc[j]));
-      acc[j] = 0.f;
-    }
-    red_add(gp + pl.off_b(0) + u, double(acc[DIN]));
-    acc[DIN] = 0.f;
-  };
-  const float* pts = static_cast<const float*>(a.pts);
-  for (long long t = ks; t < a.ntiles; t += gridDim.x) {
-    const float* Z = static_cast<const float*>(a.adj) + tc_off(a, 0, t, u / 4) + (u % 4);
-    const long long p0 = t * C::PPT;
-    for (int pt = 0; pt < C::PPT && p0 + pt < a.n; ++pt) {
-      const int row = C::row0(pt);
-      const float zv = Z[4 * row];
-#pragma unroll
-      for (int j = 0; j < DIN; ++j) {
-        acc[j] = fmaf(pts[(p0 + pt) * DIN + j], zv, acc[j]);
-        if constexpr (C::JET) acc[j] += Z[4 * (row + 1 + j)];
-      }
-      acc[DIN] += zv;
-    }
-    if (++since == 8) {
-      flush();
-      since = 0;
-    }
+// fixed-order reduction of per-tile partials into the gradient-partial rows:
+// gpart[ks][off + i] = sum over tiles t = ks, ks + KS, ... of P[t][i]
+__global__ void __launch_bounds__(256) tcw_partials_kernel(const float* __restrict__ P, int len, long long ntiles,
+                                                           double* gpart, int np_pad, int off) {
+  const int i = blockIdx.x * 256 + threadIdx.x, ks = blockIdx.y, KS = gridDim.y;
+  if (i >= len) return;
+  double acc = 0.0;
+  long long t = ks;
+  for (; t + 3 * KS < ntiles; t += 4 * KS) {
+    const float v0 = P[size_t(t) * len + i], v1 = P[size_t(t + KS) * len + i];
+    const float v2 = P[size_t(t + 2 * KS) * len + i], v3 = P[size_t(t + 3 * KS) * len + i];
+    acc += double(v0);
+    acc += double(v1);
+    acc += double(v2);
+    acc += double(v3);
   }
-  if (since) flush();
+  for (; t < ntiles; t += KS) acc += double(P[size_t(t) * len + i]);
+  gpart[size_t(ks) * np_pad + off + i] = acc;
 }
 
 }  // namespace fr

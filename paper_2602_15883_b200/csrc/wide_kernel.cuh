@@ -98,6 +98,8 @@ struct WArgs {
   int nb;                 // output units per CTA (N of the MMA)
   float* p0;              // [tiles][(DIN+1)*WP] per-tile dW_0 | db_0 partials
   float* pL;              // [tiles][WP*NOUT + NOUT] per-tile dW_L | db_L partials
+  float* st;              // [L][tiles][32][WP][4] activated S_l, row-quad major (dW operand A)
+  float* zt;              // [L][tiles][32][WP][4] Zbar_l, row-quad major (dW operand B)
 };
 
 template <typename C>

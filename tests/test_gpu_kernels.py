@@ -20,6 +20,11 @@ RE = {}
 F32_JET = 2e-5
 F32_LOSS = 2e-5
 F32_GRAD = 1e-4
+# stated TF32 tensor-core tolerances (wide FP32 experts, relative): one TF32
+# rounding (2^-11) per product, accumulated in FP32 through the layer chain
+TF32_LOSS = 5e-3
+TF32_GRAD = 5e-3
+WIDE_TAPES = (5, 6, 7)
 
 
 def _case(golden, i):
@@ -39,7 +44,7 @@ def test_jet_forward(golden, i, dtype):
     from paper_2602_15883_b200 import engine
 
     t, cfg, kind, re, _ = _case(golden, i)
-    plan = engine.get_plan(cfg, kind, re, dtype)
+    plan = engine.get_plan(cfg, kind, re, dtype, math="simt")
     y = engine.forward_jet(plan, golden[f"{t}/params"], golden[f"{t}/pts"])
     d = cfg.input_dim
     val, grad, lap = y[:, 0], np.transpose(y[:, 1 : 1 + d], (0, 2, 1)), np.transpose(y[:, 1 + d :], (0, 2, 1))
@@ -57,7 +62,7 @@ def test_pde_loss_and_gradient(golden, i, dtype):
     from paper_2602_15883_b200 import engine
 
     t, cfg, kind, re, meta = _case(golden, i)
-    plan = engine.get_plan(cfg, kind, re, dtype)
+    plan = engine.get_plan(cfg, kind, re, dtype, math="simt")
     sq, g = engine.pde_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], float(meta[3]))
     ref_sq = float(golden[f"{t}/sq_pde"])
     tol_l, tol_g = (1e-11, 1e-10) if dtype == "float64" else (F32_LOSS, F32_GRAD)
@@ -72,7 +77,7 @@ def test_mse_loss_and_gradient(golden, i, dtype):
 
     t, cfg, kind, re, meta = _case(golden, i)
     nv = cfg.output_dim - 1
-    plan = engine.get_plan(cfg, kind, re, dtype)
+    plan = engine.get_plan(cfg, kind, re, dtype, math="simt")
     su, sp, g = engine.mse_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], golden[f"{t}/tu"],
                                      golden[f"{t}/tp"], list(meta[6 : 6 + nv]), float(meta[4]), float(meta[5]))
     tol_l, tol_g = (1e-12, 1e-11) if dtype == "float64" else (F32_LOSS, F32_GRAD)
@@ -182,3 +187,82 @@ def test_reference_seam_jet_act(kind, accumulate):
     assert np.max(np.abs(st.cpu().numpy() - s_ref)) <= 1e-15
     assert np.max(np.abs(d1.cpu().numpy() - f1)) <= 1e-15
     assert max_rel(zb.cpu().numpy(), zb_ref) <= 1e-15
+
+
+@pytest.mark.parametrize("i", WIDE_TAPES)
+def test_tf32_pde_loss_and_gradient(golden, i):
+    """Wide FP32 experts on the tcgen05 TF32 path (the default math for widths
+    65..512) against the reference's float64 tapes, at the stated TF32 bound."""
+    from paper_2602_15883_b200 import engine
+
+    t, cfg, kind, re, meta = _case(golden, i)
+    plan = engine.get_plan(cfg, kind, re, "float32", math="tf32")
+    assert plan.info.math == 1
+    sq, g = engine.pde_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], float(meta[3]))
+    ref_sq = float(golden[f"{t}/sq_pde"])
+    assert abs(sq - ref_sq) <= TF32_LOSS * abs(ref_sq), (sq, ref_sq)
+    assert rel_l2(g, golden[f"{t}/grad_pde"]) < TF32_GRAD
+
+
+@pytest.mark.parametrize("i", WIDE_TAPES)
+def test_tf32_mse_loss_and_gradient(golden, i):
+    from paper_2602_15883_b200 import engine
+
+    t, cfg, kind, re, meta = _case(golden, i)
+    nv = cfg.output_dim - 1
+    plan = engine.get_plan(cfg, kind, re, "float32", math="tf32")
+    su, sp, g = engine.mse_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], golden[f"{t}/tu"],
+                                     golden[f"{t}/tp"], list(meta[6 : 6 + nv]), float(meta[4]), float(meta[5]))
+    assert abs(su - float(golden[f"{t}/sq_u"])) <= TF32_LOSS * abs(su)
+    assert abs(sp - float(golden[f"{t}/sq_p"])) <= TF32_LOSS * abs(sp)
+    assert rel_l2(g, golden[f"{t}/grad_mse"]) < TF32_GRAD
+
+
+@pytest.mark.parametrize("width,layers,act,kind", [(128, 4, "tanh", "unsteady2d"), (150, 3, "sin", "unsteady2d"),
+                                                   (96, 2, "tanh", "steady2d"), (200, 2, "sin", "unsteady3d"),
+                                                   (300, 2, "tanh", "unsteady2d")])
+def test_tf32_matches_oracle_at_cylinder_scale(width, layers, act, kind):
+    """TF32 path on cylinder-box points, including a width > 256 (two N blocks),
+    a 3D regime and the steady regime; plus bit-identical reruns."""
+    from oracle import flowrec_oracle as O
+    from paper_2602_15883_b200 import engine
+    from paper_2602_15883_b200.network import ExpertConfig, init_params
+
+    din = {"steady2d": 2, "unsteady2d": 3, "unsteady3d": 4}[kind]
+    cfg = ExpertConfig(din, layers, width, act, din if din == 4 else 3)
+    p = init_params(cfg, 3).flat
+    rng = np.random.default_rng(5)
+    n = 1000
+    cols = [rng.uniform(0, 7.35, n), rng.uniform(-7.5, 17.5, n), rng.uniform(-8, 8, n), rng.uniform(-4, 4, n)]
+    pts = np.column_stack(cols[:din] if din >= 3 else cols[1:3])
+    coef = 5.0 / n
+    sq_ref, g_ref, _ = O.pde_loss_grad(p, cfg.arch, act, kind, 100.0, pts, coef)
+    plan = engine.get_plan(cfg, kind, 100.0, "float32", math="tf32")
+    sq, g = engine.pde_loss_grad(plan, p, pts, coef)
+    assert abs(sq - sq_ref) <= TF32_LOSS * sq_ref, (sq, sq_ref)
+    assert rel_l2(g, g_ref) < TF32_GRAD
+    sq2, g2 = engine.pde_loss_grad(plan, p, pts, coef)
+    assert sq2 == sq and np.array_equal(g2, g)
+    nv = cfg.output_dim - 1
+    tu, tp = rng.standard_normal((n, nv)) * 0.1, rng.standard_normal(n) * 0.1
+    su_ref, sp_ref, gm_ref = O.mse_loss_grad(p, cfg.arch, act, pts, tu, tp, [1.0] * nv, 2.0, 3.0)
+    su, sp, gm = engine.mse_loss_grad(plan, p, pts, tu, tp, [1.0] * nv, 2.0, 3.0)
+    assert abs(su - su_ref) <= TF32_LOSS * su_ref and abs(sp - sp_ref) <= TF32_LOSS * sp_ref
+    assert rel_l2(gm, gm_ref) < TF32_GRAD
+
+
+def test_math_mode_selection():
+    """TF32 is the default for wide FP32 experts only; FP64, narrow and
+    single-hidden-layer plans refuse it."""
+    from paper_2602_15883_b200 import _lib as X
+    from paper_2602_15883_b200 import engine
+    from paper_2602_15883_b200.network import ExpertConfig
+
+    assert engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0).info.math == 1
+    assert engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0).info.math == 0
+    assert engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0, "float64").info.math == 0
+    with pytest.raises(X.FlowrecError, match="FP32"):
+        engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0, "float64", math="tf32")
+    with pytest.raises(X.FlowrecError, match="65..512"):
+        engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0, math="tf32")
+    assert engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0, math="simt").info.math == 0

@@ -12,6 +12,9 @@ pytestmark = pytest.mark.gpu
 
 F32_HIST = 1e-4
 F32_PARAMS = 1e-6
+# TF32 tensor-core path (wide experts): stated bounds after 3 epochs
+TF32_HIST = 2e-2
+TF32_PARAMS = 1e-3  # Adam normalises updates: TF32 noise on near-zero gradient components moves those params by up to ~lr per step
 
 
 def _objective(golden, tag, dtype):
@@ -122,8 +125,8 @@ def test_drop_in_worker_protocol(golden):
         assert max_rel(np.array(w.history)[:, 1:6], ref.history[r][:, 1:6]) < 1e-5
 
 
-@pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_wide_expert_training_matches_oracle(dtype):
+@pytest.mark.parametrize("dtype,math", [("float64", None), ("float32", "simt"), ("float32", "tf32")])
+def test_wide_expert_training_matches_oracle(dtype, math):
     """Hidden width > 64 runs the layer-wise kernels: a (1,1)x2 temporal split
     with [3, 96x2, 3] sin experts (two masters, anchor-normalised temporal
     messages) against the float64 oracle's serial loop."""
@@ -135,13 +138,13 @@ def test_wide_expert_training_matches_oracle(dtype):
     pb = fconfig.cylinder2d_problem(n_pde=3000, n_ghost=60, per_snapshot=12, grid_nx=9, snapshots=10,
                                     hidden_layers=2, width=96, activation="sin", counts=(1, 1), time_splits=2)
     tc = TrainConfig(epochs=3, batch_size=500, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor,
-                     lr_factor=0.5, lr_interval=2, seed=0)
+                     lr_factor=0.5, lr_interval=2, seed=0, math=math)
     plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
     res = train(plan, backend="serial", dtype=dtype)
     ranks = oracle_ranks(plan)
     hist = O.train_serial(ranks, pb.expert_config.arch, "sin", "unsteady2d", 100.0, tc.epochs, tc.lr,
                           tc.comm_interval, tc.clip_norm, tc.anchor)
-    tol_h, tol_p = (1e-9, 1e-11) if dtype == "float64" else (F32_HIST, F32_PARAMS)
+    tol_h, tol_p = {None: (1e-9, 1e-11), "simt": (F32_HIST, F32_PARAMS), "tf32": (TF32_HIST, TF32_PARAMS)}[math]
     for r in ranks:
         assert max_rel(res.history[r][:, 1:6], hist[r][:, 1:6]) < tol_h, (r, res.history[r], hist[r])
         assert rel_l2(res.params[r].flat, ranks[r]["flat"]) < tol_p
