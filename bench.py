@@ -128,6 +128,40 @@ def measure_fp32_peak(torch, X):
     return best
 
 
+def measure_tf32_peak(torch):
+    """Measured dense TF32 tensor-core throughput (TFLOP/s): cuBLAS 8192^3 FP32
+    GEMM with TF32 math (measurement only; the roofline of the tcgen05 path)."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(3):
+            a @ b
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def tc_design_bytes(L, WP, ntiles):
+    """HBM bytes one TF32 wide PDE launch moves by design: 128-row x WP fp32
+    slabs per tile (Z, Zbar, and their row-quad-major copies S^T / Zbar^T)."""
+    slabs = ((L - 1) * 2 + (L - 2)          # fwd: write Z_l and S_{l-1}^T, read Z_{l-1} (l >= 2)
+             + (L - 1) + 3 * (L - 2)        # dx: read Zbar_l; read Z_{l-1}, write Zbar_{l-1}, Zbar^T (l >= 2)
+             + 2 * (L - 1)                  # dW: read S^T and Zbar^T
+             + 4)                           # head: Z_{L-1} twice, write Zbar_{L-1} and its copy
+    return slabs * ntiles * 128 * WP * 4
+
+
 def run_ours(args):
     import torch
 
@@ -241,7 +275,8 @@ def run_ours(args):
 
     # ---- dominant kernel: the fused PDE jet-MLP fwd+bwd, timed alone ----
     pde = _time_epoch_kernel(torch, X, worker) if not worker.objective.wide else _time_wide_pde(torch, X, worker)
-    peak = measure_fp32_peak(torch, X) if rank == 0 else None
+    tf32 = worker.plan.info.math == 1 and worker.objective.wide
+    peak = (measure_tf32_peak(torch) if tf32 else measure_fp32_peak(torch, X)) if rank == 0 else None
     if dist is not None:
         dist.barrier()
 
@@ -252,6 +287,20 @@ def run_ours(args):
         fpp = flops_per_point(S=1 + rg.n_inputs + rg.n_space, L=L, W=W, d_in=rg.n_inputs, n_out=rg.n_outputs)
         flops_launch = fpp * n_loc + flops_per_value_point(L, W, rg.n_inputs, rg.n_outputs) * pde["n_mse"]
         achieved = flops_launch / pde["ms"] * 1e-9  # TFLOP/s
+        hbm = None
+        if tf32:
+            ntiles = -(-n_loc // (4 * (32 // (1 + rg.n_inputs + rg.n_space))))  # TcCfg::PPT
+            byts = tc_design_bytes(L, worker.plan.info.width_pad, ntiles)
+            peak_gbs = None
+            try:
+                with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                    peak_gbs = json.load(f).get("hbm_gbs")
+            except (OSError, ValueError):
+                pass
+            gbs = byts / (pde["ms"] * 1e-3) / 1e9
+            hbm = {"bytes_per_launch": byts, "achieved_gbs": gbs, "peak_gbs": peak_gbs,
+                   "frac": gbs / peak_gbs if peak_gbs else None,
+                   "note": "layer-wise design bytes (activation slabs through HBM); the launch is HBM-bound"}
         clk = clocks.summary()
         line = {
             "metric": METRIC,
@@ -283,17 +332,22 @@ def run_ours(args):
             "gpu_launches": (lp * args.steps) if lp is not None else None,
             "launches_per_step": lp,
             "roofline": {
-                "bound": "compute", "pipe": "fp32-simt (FFMA)",
+                "bound": "tensor" if tf32 else "compute",
+                "pipe": "tf32 tcgen05.mma (TMEM accumulators)" if tf32 else "fp32-simt (FFMA)",
                 "kernel": ("jetmlp_epoch_kernel<float,tanh,unsteady2d,64> (fr_epoch_fwd_bwd: PDE + obs/ghost heads)"
-                           if not obj.wide else "layer-wise wide kernels (fr_pde_fwd_bwd, PDE set only)"),
+                           if not obj.wide else
+                           "TF32 tcgen05 layer-wise kernels (fr_pde_fwd_bwd, PDE set only: tcw_fwd/head/dx/dw)"
+                           if tf32 else "SIMT layer-wise wide kernels (fr_pde_fwd_bwd, PDE set only)"),
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
-                "peak_source": "measured FP32 FFMA probe (fr_bench_ffma) on this GPU",
+                "peak_source": ("measured cuBLAS TF32 GEMM 8192^3 on this GPU" if tf32
+                                else "measured FP32 FFMA probe (fr_bench_ffma) on this GPU"),
                 "flops_per_point": fpp, "points_per_launch": n_loc, "value_points_per_launch": pde["n_mse"],
                 "flops_per_launch": flops_launch,
                 "kernel_ms": pde["ms"], "kernel_share_of_step": pde["ms"] / (t_rank / args.steps * 1e3),
                 "traffic": None,
             },
+            **({"hbm": hbm} if hbm else {}),
             "clocks": clk,
             "host_launches_timed": launches_host,
         }
