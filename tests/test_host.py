@@ -144,3 +144,28 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("oracles", ""), f
+
+
+@pytest.mark.parametrize("tag,kind,counts,m", [("e2d", "2d", (2, 2), 1), ("e2t", "2d", (2, 1), 2),
+                                               ("e3d", "3d", (1, 2, 1), 2)])
+def test_evaluation_ownership_bit_exact(tag, kind, counts, m):
+    """Owner of every evaluation point == the reference's stitch() owners
+    (half-open floor rule, decomposition.py:259-286); masters likewise."""
+    import os
+
+    from paper_2602_15883_b200 import benchmarks
+    from paper_2602_15883_b200.decomposition import GlobalDomain, identify_masters, owner_ranks, partition
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_eval.npz"))
+    if kind == "2d":
+        sol = benchmarks.TaylorGreen2D(re=100.0, spatial_box=((-7.5, 17.5), (-8.0, 8.0)), time_interval=(0.0, 7.35))
+    else:
+        sol = benchmarks.Beltrami3D(a=1.0, d=1.0, re=300.0, spatial_box=((-5.0, 20.0), (-5.0, 5.0), (0.0, 10.0)),
+                                    time_interval=(0.0, 11.85))
+    domain = GlobalDomain.from_solution(sol)
+    subs = partition(domain, counts, m, delta_space=2.0, delta_time=1.0)
+    assert np.array_equal(owner_ranks(domain, counts, m, g[f"{tag}/points"]), g[f"{tag}/owners"])
+    assert np.array_equal(np.array(benchmarks.grid_points(sol, 17 if kind == "2d" else 7, 8 if kind == "2d" else 4)),
+                          g[f"{tag}/points"])
+    anchor = tuple(g[f"{tag}/anchor"])
+    assert sorted(identify_masters(subs, anchor)) == [int(r) for r in g[f"{tag}/masters"]]
