@@ -148,3 +148,38 @@ def test_wide_expert_training_matches_oracle(dtype, math):
     for r in ranks:
         assert max_rel(res.history[r][:, 1:6], hist[r][:, 1:6]) < tol_h, (r, res.history[r], hist[r])
         assert rel_l2(res.params[r].flat, ranks[r]["flat"]) < tol_p
+
+
+def test_resume_from_training_state_is_bit_identical(tmp_path):
+    """FRTS state files (params, Adam moments, step, history, ghost targets) let
+    a fresh LocalTrainer continue exactly: 2 + save/load + 2 epochs == 4 epochs;
+    FRCK checkpoints written from the device buffers load back exactly."""
+    from paper_2602_15883_b200 import checkpoint as ck
+    from paper_2602_15883_b200 import config as fconfig
+    from paper_2602_15883_b200.runtime import TrainConfig, build_plan
+    from paper_2602_15883_b200.runtime.driver import LocalTrainer
+
+    pb = fconfig.cylinder2d_problem(n_pde=2000, n_ghost=40, per_snapshot=12, grid_nx=9, snapshots=10,
+                                    hidden_layers=2, width=32, activation="tanh", counts=(2, 1), time_splits=2)
+    tc = TrainConfig(epochs=4, batch_size=500, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor,
+                     lr_factor=0.5, lr_interval=2, comm_interval=3, seed=0)  # epoch 2 reuses saved targets
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
+    full = LocalTrainer(plan)
+    full.run(4)
+    a = LocalTrainer(plan)
+    a.run(2)
+    ck.save_trainer_state(tmp_path / "st", a)
+    b = LocalTrainer(plan)
+    start = ck.load_trainer_state(tmp_path / "st", b)
+    assert start == 2
+    b.run(2, start=start)
+    for r in full.workers:
+        wf, wb = full.workers[r], b.workers[r]
+        assert np.array_equal(wf.flat.cpu().numpy(), wb.flat.cpu().numpy()), r
+        wf.sync_history()
+        wb.sync_history()
+        assert np.array_equal(np.array(wf.history)[:, 1:], np.array(wb.history)[:, 1:]), r
+        path = tmp_path / f"r{r}.frck"
+        ck.save_checkpoint_device(path, plan.expert_config, wb.flat, seed=wb.ws.param_seed)
+        q = ck.load_checkpoint(path)
+        assert np.array_equal(q.flat, wb.flat.cpu().numpy()) and q.seed == wb.ws.param_seed
