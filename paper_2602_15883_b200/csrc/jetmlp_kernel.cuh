@@ -178,6 +178,7 @@ struct JetCfg {
     if (BWD) e += al(ROWS * NOUT);         // Ybs
     e += al(PPT * DIN);                    // Ps
     if (MODE == MODE_MSE) e += al(PPT * NVEL) + al(PPT);  // targets
+    if (BWD) e += al(NT);                  // db partials
     return e;
   }
   __host__ __device__ static size_t smem_bytes(int L) {
@@ -215,7 +216,7 @@ __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __re
     for (int j = 0; j < 8; ++j) acc[r][j] = T(0);
   const T* ap = A + rg * (4 * RPT);
   const T* bp = B + 4 * g;
-#pragma unroll 2
+#pragma unroll 8
   for (int kq = 0; kq < W / 4; ++kq) {
     T av[4 * RPT];
     vload(av, ap + kq * RS4);
@@ -294,6 +295,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   T* Ybs = nullptr;
   if constexpr (BWD) { Ybs = sm; sm += C::al(ROWS * NOUT); }
   T* Ps = sm;                      sm += C::al(PPT * DIN);
+  T* Dbs = nullptr;
+  if constexpr (BWD) { Dbs = sm; sm += C::al(NT); }
   T* TUs = nullptr;
   T* TPs = nullptr;
   if constexpr (MODE == MODE_MSE) {
@@ -758,7 +761,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             const T* x1 = Xs + (kt + KT) * RS4 + 4 * (rs * RROWS);
             const T* z0 = Gs + ut * RS4 + 4 * (rs * RROWS);
             const T* z1 = Gs + (ut + KT) * RS4 + 4 * (rs * RROWS);
-#pragma unroll 2
+#pragma unroll 4
             for (int r = 0; r < RROWS; ++r) {
               T h[8], z[8];
               vload(*reinterpret_cast<T(*)[4]>(h), x0 + 4 * r);
@@ -771,10 +774,14 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                 for (int y = 0; y < 8; ++y) acc[x][y] = fma(h[x], z[y], acc[x][y]);
             }
           }
-          if (tid < W) {
+          {
+            // db_l partials: thread = (unit, point phase); combined below in phase order
+            constexpr int NH = NT / W;
+            static_assert(NT % W == 0, "db split needs NT % W == 0");
+            const int u = tid % W, h = tid / W;
             T sb = T(0);
-            for (int pt = 0; pt < PPT; ++pt) sb += Gs[kqi<RS4>(JET ? pt * S : pt, tid)];
-            red_add(gp + pl.off_b(l) + tid, double(sb));
+            for (int pt = h; pt < PPT; pt += NH) sb += Gs[kqi<RS4>(JET ? pt * S : pt, u)];
+            Dbs[tid] = sb;
           }
           __syncthreads();  // every read of Xs (H_l) is done: reuse it as scratch
           FR_MARK(8);
@@ -792,6 +799,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           }
           FR_MARK(9);
           __syncthreads();
+          if (tid < W) {
+            T sb = Dbs[tid];
+#pragma unroll
+            for (int h = 1; h < NT / W; ++h) sb += Dbs[h * W + tid];
+            red_add(gp + pl.off_b(l) + tid, double(sb));
+          }
           {
             double* dst = gp + pl.off_w(l);
             for (int e = tid; e < W * W; e += NT) {
