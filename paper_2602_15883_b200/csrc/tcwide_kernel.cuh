@@ -237,15 +237,20 @@ __device__ __forceinline__ const float* tc_wslab(const WArgs& a, long long base,
 
 // ---------------------------------------------------------------------------
 // forward, hidden layer l >= 1: Z_l = sigma(Z_{l-1}) W_l + b_l
-// grid (tiles, WP/NB), 128 threads.  Ring stage = Z_{l-1} slab (8 KB, activated
-// in place) + W_l^T slab (NB x 16).
+// grid (tiles, WP/NB), 320 threads, warp specialised over a TC_NS-stage ring
+// (stage = Z_{l-1} slab of 4 unit quads x 128 rows + W_l^T slab NB x 16):
+//   warp 4      loader: bulk copies once the stage's MMA and St store are done
+//   warps 0..3  jet activation in place (smem), then the TMEM -> Z_l epilogue
+//   warp 5      MMA issuer (2 K-steps per stage), commit frees the stage
+//   warps 6..9  S_{l-1} row-quad-major copy for dW (N block 0 only)
 // ---------------------------------------------------------------------------
+constexpr int TC_FWD_NT = 320;
 template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_fwd_kernel(WArgs a, int l) {
+__global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
   using C = TcCfg<ACT, MODE, REG>;
   extern __shared__ __align__(128) unsigned char tc_smem[];
   float* ring = reinterpret_cast<float*>(tc_smem);
-  __shared__ __align__(8) uint64_t full[TC_NS], empty[TC_NS];
+  __shared__ __align__(8) uint64_t full[TC_NS], actd[TC_NS], mmad[TC_NS], std_[TC_NS];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long tile = blockIdx.x;
@@ -253,74 +258,96 @@ __global__ void __launch_bounds__(128) tcw_fwd_kernel(WArgs a, int l) {
   const float* kp = static_cast<const float*>(a.kp);
   const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
   if (tid == 0)
-    for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
-  const uint32_t tmem = tc_setup<256>(&tslot, empty, TC_NS);
+    for (int i = 0; i < TC_NS; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&actd[i], 4);
+      tc::mbar_init(&std_[i], 4);
+    }
+  const uint32_t tmem = tc_setup<256>(&tslot, mmad, TC_NS);
   const int nch = a.WP / TC_KC;
   const bool virt = (l == 1);
   const size_t SF = C::stage_floats(NB);
-  const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, 0));
-  auto produce = [&](int c) {
-    const int s = c % TC_NS;
-    float* st = ring + s * SF;
-    tc::mbar_expect_tx(&full[s], NB * 64 + (virt ? 0 : 8192));
-    tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
-    if (!virt) tc::bulk_g2s(st, zsrc + size_t(c) * 2048, 8192, &full[s]);
+  auto arrive = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
   };
-  if (tid == 0)
-    for (int c = 0; c < TC_NS && c < nch; ++c) produce(c);
-  const uint32_t idesc = tc::idesc_tf32(128, NB);
-  for (int c = 0; c < nch; ++c) {
-    const int s = c % TC_NS;
-    float* A = ring + s * SF;
-    tc::mbar_wait(&full[s], (c / TC_NS) & 1);
-    for (int i = tid; i < C::ITEMS; i += C::NT) {
-      const int pt = i % C::PPT, kq = i / C::PPT;
-      float z[C::S][4], sv[C::S][4];
-      if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, 4 * c + kq, z);
-      else slab_load<C>(z, A, pt, kq);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float zz[C::S], ss[C::S];
-        col<C>(z, j, zz);
-        tc_act1<C, ACT>(zz, ss);
-#pragma unroll
-        for (int k = 0; k < C::S; ++k) sv[k][j] = ss[k];
-      }
-      slab_store<C>(A, pt, kq, sv);
-    }
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      tc_mma16(tmem, A, 128, A + 2048, NB, idesc, c == 0);
-      tc::mma_commit(&empty[s]);
-      // refill the stage of the previous chunk once its MMAs have drained
-      if (c >= 1 && c - 1 + TC_NS < nch) {
-        tc::mbar_wait(&empty[(c - 1) % TC_NS], ((c - 1) / TC_NS) & 1);
-        produce(c - 1 + TC_NS);
+  if (warp == 4) {
+    if (lane == 0) {
+      const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, 0));
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % TC_NS;
+        if (c >= TC_NS) {
+          const uint32_t ph = ((c - TC_NS) / TC_NS) & 1;
+          tc::mbar_wait(&mmad[s], ph);
+          tc::mbar_wait(&std_[s], ph);
+        }
+        float* st = ring + s * SF;
+        tc::mbar_expect_tx(&full[s], NB * 64 + (virt ? 0 : 8192));
+        tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
+        if (!virt) tc::bulk_g2s(st, zsrc + size_t(c) * 2048, 8192, &full[s]);
       }
     }
-    // S_{l-1} row-quad major for the weight gradient (the N block 0 CTA writes it)
-#ifndef FR_NO_ST
-    if (nb == 0) slab_store_t<C>(A, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, tid);
-#endif
-  }
-  tc::mbar_wait(&empty[(nch - 1) % TC_NS], ((nch - 1) / TC_NS) & 1);
-  tc::fence_after();
-  const int r = warp * 32 + lane;
-  const bool vrow = lane < C::VR && (lane % C::S) == 0;
-  float* Zo = static_cast<float*>(a.act) + tc_off(a, l, tile, n0 / 4) + r * 4;
-  const float* bl = kp + pl.off_b(l) + n0;
-  for (int c0 = 0; c0 < NB; c0 += 16) {
-    float v[16];
-    tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
-    if (vrow)
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, NB);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % TC_NS;
+        float* A = ring + s * SF;
+        tc::mbar_wait(&actd[s], (c / TC_NS) & 1);
+        tc::fence_after();
+        tc_mma16(tmem, A, 128, A + 2048, NB, idesc, c == 0);
+        tc::mma_commit(&mmad[s]);
+      }
+    }
+  } else if (warp >= 6) {
+    const int t = tid - 192;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % TC_NS;
+      tc::mbar_wait(&actd[s], (c / TC_NS) & 1);
+      if (nb == 0) slab_store_t<C>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
+      arrive(&std_[s]);
+    }
+  } else {
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % TC_NS;
+      float* A = ring + s * SF;
+      tc::mbar_wait(&full[s], (c / TC_NS) & 1);
+      for (int i = tid; i < C::ITEMS; i += 128) {
+        const int pt = i % C::PPT, kq = i / C::PPT;
+        float z[C::S][4], sv[C::S][4];
+        if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, 4 * c + kq, z);
+        else slab_load<C>(z, A, pt, kq);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] += bl[c0 + i];
+        for (int j = 0; j < 4; ++j) {
+          float zz[C::S], ss[C::S];
+          col<C>(z, j, zz);
+          tc_act1<C, ACT>(zz, ss);
 #pragma unroll
-    for (int h = 0; h < 4; ++h)
-      *reinterpret_cast<float4*>(Zo + size_t(c0 / 4 + h) * 512) =
-          make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+          for (int k = 0; k < C::S; ++k) sv[k][j] = ss[k];
+        }
+        slab_store<C>(A, pt, kq, sv);
+      }
+      tc::fence_proxy_async();
+      arrive(&actd[s]);
+    }
+    // epilogue: Z_l = D + b on value rows
+    tc::mbar_wait(&mmad[(nch - 1) % TC_NS], ((nch - 1) / TC_NS) & 1);
+    tc::fence_after();
+    const int r = warp * 32 + lane;
+    const bool vrow = lane < C::VR && (lane % C::S) == 0;
+    float* Zo = static_cast<float*>(a.act) + tc_off(a, l, tile, n0 / 4) + r * 4;
+    const float* bl = kp + pl.off_b(l) + n0;
+    for (int c0 = 0; c0 < NB; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+      if (vrow)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += bl[c0 + i];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        *reinterpret_cast<float4*>(Zo + size_t(c0 / 4 + h) * 512) =
+            make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+    }
   }
   tc_teardown<256>(tmem);
 }
