@@ -29,7 +29,7 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   const dim3 gt(a.ntiles, a.WP / NB);
   for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, TC_FWD_NT, C::gemm_smem(NB), st>>>(a, l);
   tcw_head_kernel<ACT, MODE, REG><<<a.ntiles, C::NT, C::head_smem(a.WP), st>>>(a);
-  for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, C::NT, C::gemm_smem(NB), st>>>(a, l);
+  for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, TC_DX_NT, C::gemm_smem(NB), st>>>(a, l);
   // dW: all ceil(WP/128) k-blocks of an N block accumulate in TMEM (<= 512
   // columns); N block = the largest multiple of 16 dividing WP that fits
   const int nkb = (a.WP + 127) / 128;

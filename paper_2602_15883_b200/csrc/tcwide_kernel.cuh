@@ -354,19 +354,23 @@ __global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
 
 // ---------------------------------------------------------------------------
 // adjoint, hidden layer l >= 1: Zbar_{l-1} = act_bwd(Z_{l-1}, Zbar_l W_l^T)
-// grid (tiles, WP/NB), 128 threads.  Main loop: one thread streams Zbar_l and
-// W_l slabs and issues the MMAs.  Epilogue (16 columns at a time): TMEM ->
-// shared S-bar slab, Z_{l-1} slab prefetched by bulk copy, point-major act-bwd.
-// For l == 1 the layer-0 adjoint is reduced straight into per-tile dW_0 | db_0
-// partials (Zbar_0 is never stored).
+// grid (tiles, WP/NB), 256 threads.  Main loop: thread 0 streams Zbar_l and W_l
+// slabs through the ring and issues the MMAs.  Epilogue, 16 TMEM columns per
+// step with double-buffered staging: warps 0..3 move S-bar TMEM -> shared,
+// prefetch the Z_{l-1} slab (bulk copy) and run the point-major act-bwd in
+// place; warps 4..7 meanwhile write the previous step's Zbar_{l-1} slab to HBM
+// in both layouts (k-quad for the next adjoint, row-quad for dW).  For l == 1
+// the layer-0 adjoint is reduced straight into per-tile dW_0 | db_0 partials
+// (Zbar_0 is never stored).
 // ---------------------------------------------------------------------------
+constexpr int TC_DX_NT = 256;
 template <int ACT, int MODE, int REG>
-__global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l) {
+__global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
   using C = TcCfg<ACT, MODE, REG>;
   constexpr int DIN = C::DIN, D1 = DIN + 1;
   extern __shared__ __align__(128) unsigned char tc_smem[];
   float* ring = reinterpret_cast<float*>(tc_smem);
-  __shared__ __align__(8) uint64_t full[TC_NS], empty[TC_NS], zfull[2];
+  __shared__ __align__(8) uint64_t full[TC_NS], empty[TC_NS], zfull[2], rdy[2], done[2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long tile = blockIdx.x;
@@ -375,8 +379,11 @@ __global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l) {
   const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
   if (tid == 0) {
     for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
-    tc::mbar_init(&zfull[0], 1);
-    tc::mbar_init(&zfull[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&zfull[i], 1);
+      tc::mbar_init(&rdy[i], 4);
+      tc::mbar_init(&done[i], 4);
+    }
   }
   const uint32_t tmem = tc_setup<256>(&tslot, empty, TC_NS);
   const int nch = a.WP / TC_KC;
@@ -409,90 +416,108 @@ __global__ void __launch_bounds__(128) tcw_dx_kernel(WArgs a, int l) {
   tc::fence_after();
   __syncthreads();  // every thread is past the ring before it is reused
   // epilogue buffers inside the (now idle) ring
-  float* stg = ring;             // [4][128][4]  S-bar columns
-  float* zc = ring + 2048;       // [2][4][128][4] Z_{l-1} slabs
-  float* red = ring + 3 * 2048;  // [PPT][4 kq][4 j][D1] dW_0 contributions
+  float* stg = ring;             // [2][4][128][4]  S-bar / Zbar columns
+  float* zc = ring + 2 * 2048;   // [2][4][128][4]  Z_{l-1} slabs
   const bool virt = (l == 1);
+  float* red = ring + 2048;      // [PPT][4 kq][4 j][D1] dW_0 contributions (l == 1: stg[1], zc unused)
   const int nck = NB / 16;
   const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, n0 / 4));
-  if (!virt && tid == 0)
-    for (int j = 0; j < 2 && j < nck; ++j) {
-      tc::mbar_expect_tx(&zfull[j], 8192);
-      tc::bulk_g2s(zc + j * 2048, zsrc + size_t(j) * 2048, 8192, &zfull[j]);
-    }
-  const int r = warp * 32 + lane;
-  const float* pts = static_cast<const float*>(a.pts);
-  for (int j = 0; j < nck; ++j) {
-    {
-      float v[16];
-      tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16 * j, v);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float4*>(stg + q * 512 + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    }
-    __syncthreads();
-    if (!virt) tc::mbar_wait(&zfull[j & 1], (j >> 1) & 1);
-    const float* zs = zc + (j & 1) * 2048;
-    for (int i = tid; i < C::ITEMS; i += C::NT) {
-      const int pt = i % C::PPT, kq = i / C::PPT;
-      const int q = n0 / 4 + 4 * j + kq;
-      float z[C::S][4], sb[C::S][4];
-      if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
-      else slab_load<C>(z, zs, pt, kq);
-      slab_load<C>(sb, stg, pt, kq);
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        float zz[C::S], bb[C::S], sa[C::S];
-        col<C>(z, jj, zz);
-        col<C>(sb, jj, bb);
-        tc_act_bwd1<C, ACT>(zz, bb, sa);
-#pragma unroll
-        for (int k = 0; k < C::S; ++k) sb[k][jj] = bb[k];
+  auto arrive = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+  };
+  auto sync_e = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+  if (tid < 128) {
+    if (!virt && tid == 0)
+      for (int j = 0; j < 2 && j < nck; ++j) {
+        tc::mbar_expect_tx(&zfull[j], 8192);
+        tc::bulk_g2s(zc + j * 2048, zsrc + size_t(j) * 2048, 8192, &zfull[j]);
       }
-      if (!virt) {
-        slab_store<C>(stg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
-      } else {
-        // dW_0[i][u] += x_i zbar_v + zbar_{g_i} ; db_0[u] += zbar_v (zero for padding points)
-        const long long p = tile * C::PPT + pt;
-        const bool live = p < a.n;
-        float x[DIN];
+    const int r = warp * 32 + lane;
+    const float* pts = static_cast<const float*>(a.pts);
+    for (int j = 0; j < nck; ++j) {
+      const int b = virt ? 0 : (j & 1);
+      float* sg = stg + b * 2048;
+      if (!virt && j >= 2) tc::mbar_wait(&done[b], ((j - 2) >> 1) & 1);
+      {
+        float v[16];
+        tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16 * j, v);
 #pragma unroll
-        for (int ii = 0; ii < DIN; ++ii) x[ii] = live ? pts[p * DIN + ii] : 0.f;
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(sg + q * 512 + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      sync_e();
+      if (!virt) tc::mbar_wait(&zfull[b], (j >> 1) & 1);
+      const float* zs = zc + b * 2048;
+      for (int i = tid; i < C::ITEMS; i += 128) {
+        const int pt = i % C::PPT, kq = i / C::PPT;
+        const int q = n0 / 4 + 4 * j + kq;
+        float z[C::S][4], sb[C::S][4];
+        if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
+        else slab_load<C>(z, zs, pt, kq);
+        slab_load<C>(sb, sg, pt, kq);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
-          const float zv = live ? sb[0][jj] : 0.f;
+          float zz[C::S], bb[C::S], sa[C::S];
+          col<C>(z, jj, zz);
+          col<C>(sb, jj, bb);
+          tc_act_bwd1<C, ACT>(zz, bb, sa);
 #pragma unroll
-          for (int ii = 0; ii < DIN; ++ii) {
-            float t = x[ii] * zv;
-            if constexpr (C::JET) t += live ? sb[1 + ii][jj] : 0.f;
-            rd[ii] = t;
+          for (int k = 0; k < C::S; ++k) sb[k][jj] = bb[k];
+        }
+        if (!virt) {
+          slab_store<C>(sg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
+        } else {
+          // dW_0[i][u] += x_i zbar_v + zbar_{g_i} ; db_0[u] += zbar_v (zero for padding points)
+          const long long p = tile * C::PPT + pt;
+          const bool live = p < a.n;
+          float x[DIN];
+#pragma unroll
+          for (int ii = 0; ii < DIN; ++ii) x[ii] = live ? pts[p * DIN + ii] : 0.f;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+            const float zv = live ? sb[0][jj] : 0.f;
+#pragma unroll
+            for (int ii = 0; ii < DIN; ++ii) {
+              float t = x[ii] * zv;
+              if constexpr (C::JET) t += live ? sb[1 + ii][jj] : 0.f;
+              rd[ii] = t;
+            }
+            rd[DIN] = zv;
           }
-          rd[DIN] = zv;
         }
       }
-    }
-    __syncthreads();
-    if (!virt) {
-      if (tid == 0 && j + 2 < nck) {
-        tc::mbar_expect_tx(&zfull[j & 1], 8192);
-        tc::bulk_g2s(zc + (j & 1) * 2048, zsrc + size_t(j + 2) * 2048, 8192, &zfull[j & 1]);
-      }
-      slab_copy_out(stg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), tid);
-#ifndef FR_NO_ST
-      slab_store_t<C>(stg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, tid);
-#endif
-    } else {
-      // fixed-order sum over the tile's points -> p0[tile][i*WP + u] (i == DIN: db_0)
-      for (int e = tid; e < 16 * D1; e += C::NT) {
-        const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
-        float acc = 0.f;
-        for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + jj) * D1 + ii];
-        const int u = n0 + 16 * j + 4 * kq + jj;
-        a.p0[size_t(tile) * (D1 * a.WP) + size_t(ii) * a.WP + u] = acc;
+      sync_e();
+      if (!virt) {
+        if (tid == 0 && j + 2 < nck) {
+          tc::mbar_expect_tx(&zfull[b], 8192);
+          tc::bulk_g2s(zc + b * 2048, zsrc + size_t(j + 2) * 2048, 8192, &zfull[b]);
+        }
+        arrive(&rdy[b]);
+      } else {
+        // fixed-order sum over the tile's points -> p0[tile][i*WP + u] (i == DIN: db_0)
+        for (int e = tid; e < 16 * D1; e += 128) {
+          const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
+          float acc = 0.f;
+          for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + jj) * D1 + ii];
+          const int u = n0 + 16 * j + 4 * kq + jj;
+          a.p0[size_t(tile) * (D1 * a.WP) + size_t(ii) * a.WP + u] = acc;
+        }
+        sync_e();
       }
     }
-    __syncthreads();
+  } else if (!virt) {
+    // writer warps: Zbar_{l-1} slab j in both HBM layouts
+    const int t = tid - 128;
+    for (int j = 0; j < nck; ++j) {
+      const int b = j & 1;
+      tc::mbar_wait(&rdy[b], (j >> 1) & 1);
+      const float* sg = stg + b * 2048;
+      slab_copy_out(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
+      slab_store_t<C>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+      arrive(&done[b]);
+    }
   }
   tc_teardown<256>(tmem);
 }
