@@ -206,10 +206,72 @@ __device__ __forceinline__ int unit_of(int g, int j) {
 // same fixed-order sum on every run.
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
 
+// ---------------------------------------------------------------------------
+// packed FP32 pairs (sm_100a FFMA2: fma.rn.f32x2, one issue slot for two FMAs).
+// Each lane is an ordinary fma.rn.f32, so results are bit-identical to FFMA;
+// the point is halving the issue slots the FP32 contractions take, which frees
+// the dispatcher for the LDS / address / epilogue instructions in between.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2_pack(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+// d.{x,y} = fma(a, b.{x,y}, d.{x,y})  (scalar a broadcast: FFMA2 R, Ra.F32, Rb.F32x2, Rd.F32x2)
+__device__ __forceinline__ void f2_fma(f32x2& d, float a, f32x2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(f2_pack(a, a)), "l"(b));
+}
+// two pairs from 16 aligned bytes of shared memory
+__device__ __forceinline__ void f2_lds(f32x2& p0, f32x2& p1, const float* src) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src);
+  p0 = v.x;
+  p1 = v.y;
+}
+
 // acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][unit_of(g, j)]
 template <typename T, int W, int RPT, int RS4>
 __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
                                           T (&acc)[RPT][8]) {
+  if constexpr (sizeof(T) == 4) {
+    // FP32: unit pairs (0,1) (2,3) (4,5) (6,7) accumulate as FFMA2 with the row
+    // activation broadcast; same per-element fma chain (k ascending) as below
+    f32x2 acc2[RPT][4];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc2[r][q] = 0ull;
+    const float* ap = reinterpret_cast<const float*>(A) + rg * (4 * RPT);
+    const float* bp = reinterpret_cast<const float*>(B) + 4 * g;
+#pragma unroll 8
+    for (int kq = 0; kq < W / 4; ++kq) {
+      float av[4 * RPT];
+      vload(av, ap + kq * RS4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        f32x2 b[4];
+        f2_lds(b[0], b[1], bp + (4 * kq + kk) * W);
+        f2_lds(b[2], b[3], bp + (4 * kq + kk) * W + W / 2);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) f2_fma(acc2[r][q], av[4 * r + kk], b[q]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float x, y;
+        f2_unpack(acc2[r][q], x, y);
+        acc[r][2 * q] = T(x);
+        acc[r][2 * q + 1] = T(y);
+      }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -756,7 +818,42 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           for (int x = 0; x < 8; ++x)
 #pragma unroll
             for (int y = 0; y < 8; ++y) acc[x][y] = T(0);
-          if (active) {
+          if constexpr (sizeof(T) == 4) {
+            // FP32: unit pairs as FFMA2 (H broadcast), same fma chain order
+            if (active) {
+              const float* x0 = reinterpret_cast<const float*>(Xs) + kt * RS4 + 4 * (rs * RROWS);
+              const float* x1 = reinterpret_cast<const float*>(Xs) + (kt + KT) * RS4 + 4 * (rs * RROWS);
+              const float* z0 = reinterpret_cast<const float*>(Gs) + ut * RS4 + 4 * (rs * RROWS);
+              const float* z1 = reinterpret_cast<const float*>(Gs) + (ut + KT) * RS4 + 4 * (rs * RROWS);
+              f32x2 acc2[8][4];
+#pragma unroll
+              for (int x = 0; x < 8; ++x)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc2[x][q] = 0ull;
+#pragma unroll 4
+              for (int r = 0; r < RROWS; ++r) {
+                float h[8];
+                f32x2 z[4];
+                vload(*reinterpret_cast<float(*)[4]>(h), x0 + 4 * r);
+                vload(*reinterpret_cast<float(*)[4]>(h + 4), x1 + 4 * r);
+                f2_lds(z[0], z[1], z0 + 4 * r);
+                f2_lds(z[2], z[3], z1 + 4 * r);
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) f2_fma(acc2[x][q], h[x], z[q]);
+              }
+#pragma unroll
+              for (int x = 0; x < 8; ++x)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float a0, a1;
+                  f2_unpack(acc2[x][q], a0, a1);
+                  acc[x][2 * q] = T(a0);
+                  acc[x][2 * q + 1] = T(a1);
+                }
+            }
+          } else if (active) {
             const T* x0 = Xs + kt * RS4 + 4 * (rs * RROWS);
             const T* x1 = Xs + (kt + KT) * RS4 + 4 * (rs * RROWS);
             const T* z0 = Gs + ut * RS4 + 4 * (rs * RROWS);
@@ -934,9 +1031,11 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE, REG, W>::NT, 1) jetmlp_ke
 }
 
 // A whole epoch's loss heads in one persistent launch: every CTA first walks its
-// static share of PDE tiles, then MSE tiles (obs, ghost-spatial, ghost-temporal)
-// dealt out from the last CTA backwards, i.e. to the CTAs that got one PDE tile
-// fewer.  Assignment is static, so the per-CTA partial sums -- and the reduced
+// static share of PDE tiles, then the MSE tiles (obs, ghost-spatial,
+// ghost-temporal) continue the same round robin: global tile index
+// offset + t goes to CTA (offset + t) mod G, so the first MSE tiles land on the
+// CTAs that got one PDE tile fewer and no CTA holds more than ceil(total / G)
+// tiles.  Assignment is static, so the per-CTA partial sums -- and the reduced
 // loss and gradient -- are identical on every run.
 struct EpochArgs {
   KArgs pde;
@@ -953,7 +1052,7 @@ __global__ void __launch_bounds__(JetCfg<T, ACT, MODE_PDE, REG, W>::NT, 1) jetml
   run_tiles<T, ACT, MODE_PDE, REG, W, NT>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c);
   long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W>::PPT;
   for (int d = 0; d < e.n_mse; ++d) {
-    const long long t0 = (((G - 1 - c) - offset) % G + G) % G;
+    const long long t0 = ((c - offset) % G + G) % G;
     run_tiles<T, ACT, MODE_MSE, REG, W, NT>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c);
     offset += (e.mse[d].n + JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT;
   }
