@@ -386,7 +386,10 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       for (int i = tid; i < a.np_pad; i += NT) gp[i] = 0.0;
   }
   T* stash = static_cast<T*>(a.scratch) + size_t(blockIdx.x) * a.stash_elems;
-  auto st_idx = [&](int layer, int q) { return (C::stash_layer_base(layer) + q) * NT + tid; };
+  // stash element q of `layer` for this thread lives at st_at(layer)[q * NT]:
+  // one 64-bit base per layer, every q an immediate offset (coalesced over tid)
+  T* const stash_t = stash + tid;
+  auto st_at = [&](int layer) { return stash_t + size_t(C::stash_layer_base(layer)) * NT; };
 
   double lacc0 = 0.0, lacc1 = 0.0;
 
@@ -466,8 +469,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             outv[pr][j] = s;
           }
           if constexpr (BWD) {
-            stash[st_idx(0, (pr * 8 + j) * NST0)] = s;
-            if constexpr (C::SIN) stash[st_idx(0, (pr * 8 + j) * NST0 + 1)] = c;
+            st_at(0)[((pr * 8 + j) * NST0) * NT] = s;
+            if constexpr (C::SIN) st_at(0)[((pr * 8 + j) * NST0 + 1) * NT] = c;
           }
         }
       }
@@ -506,14 +509,14 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             const int q = j * NSTH;
             const T d3 = act_d3<ACT>(s, c, d1, d2);
 #pragma unroll
-            for (int st = 0; st < S; ++st) stash[st_idx(l, q + st)] = outv[st][j];
-            stash[st_idx(l, q + S)] = d1;
+            for (int st = 0; st < S; ++st) st_at(l)[(q + st) * NT] = outv[st][j];
+            st_at(l)[(q + S) * NT] = d1;
 #pragma unroll
-            for (int i = 0; i < NG; ++i) stash[st_idx(l, q + S + 1 + i)] = d2 * acc[1 + i][j];
+            for (int i = 0; i < NG; ++i) st_at(l)[(q + S + 1 + i) * NT] = d2 * acc[1 + i][j];
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
               const T zg = acc[1 + LAP0 + i][j];
-              stash[st_idx(l, q + S + 1 + NG + i)] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
+              st_at(l)[(q + S + 1 + NG + i) * NT] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
             }
           }
         } else {
@@ -524,8 +527,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             act_eval<ACT>(zv, s, c);
             outv[r][j] = s;
             if constexpr (BWD) {
-              stash[st_idx(l, (r * 8 + j) * NST0)] = s;
-              if constexpr (C::SIN) stash[st_idx(l, (r * 8 + j) * NST0 + 1)] = c;
+              st_at(l)[((r * 8 + j) * NST0) * NT] = s;
+              if constexpr (C::SIN) st_at(l)[((r * 8 + j) * NST0 + 1) * NT] = c;
             }
           }
         }
@@ -735,12 +738,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             if constexpr (JET) {
               // numpy_backend.py:58-89 with the forward-time factors
               const int q = j * NSTH + S;
-              const T d1 = stash[st_idx(l, q)];
+              const T d1 = st_at(l)[(q) * NT];
               T ga[NG], lb[NL > 0 ? NL : 1];
 #pragma unroll
-              for (int i = 0; i < NG; ++i) ga[i] = stash[st_idx(l, q + 1 + i)];
+              for (int i = 0; i < NG; ++i) ga[i] = st_at(l)[(q + 1 + i) * NT];
 #pragma unroll
-              for (int i = 0; i < NL; ++i) lb[i] = stash[st_idx(l, q + 1 + NG + i)];
+              for (int i = 0; i < NL; ++i) lb[i] = st_at(l)[(q + 1 + NG + i) * NT];
               T zv = sb[0][j] * d1;
 #pragma unroll
               for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * ga[i];
@@ -758,8 +761,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             } else {
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
-                const T s = stash[st_idx(l, (r * 8 + j) * NST0)];
-                const T c = C::SIN ? stash[st_idx(l, (r * 8 + j) * NST0 + 1)] : T(0);
+                const T s = st_at(l)[((r * 8 + j) * NST0) * NT];
+                const T c = C::SIN ? st_at(l)[((r * 8 + j) * NST0 + 1) * NT] : T(0);
                 T d1, d2;
                 act_d12<ACT>(s, c, d1, d2);
                 zb[r][j] = sb[r][j] * d1;
@@ -777,8 +780,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             const int u = unit_of<W>(g, j);
             if constexpr (JET) {
               if (lp == 0) {
-                const T s = stash[st_idx(0, j * NST0)];
-                const T c = C::SIN ? stash[st_idx(0, j * NST0 + 1)] : T(0);
+                const T s = st_at(0)[(j * NST0) * NT];
+                const T c = C::SIN ? st_at(0)[(j * NST0 + 1) * NT] : T(0);
                 T d1, d2;
                 act_d12<ACT>(s, c, d1, d2);
                 hv[0][j] = s;
@@ -791,11 +794,11 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                 }
               } else {
 #pragma unroll
-                for (int st = 0; st < S; ++st) hv[st][j] = stash[st_idx(lp, j * NSTH + st)];
+                for (int st = 0; st < S; ++st) hv[st][j] = st_at(lp)[(j * NSTH + st) * NT];
               }
             } else {
 #pragma unroll
-              for (int r = 0; r < RPT; ++r) hv[r][j] = stash[st_idx(lp, (r * 8 + j) * NST0)];
+              for (int r = 0; r < RPT; ++r) hv[r][j] = st_at(lp)[((r * 8 + j) * NST0) * NT];
             }
           }
           store_block<T, W, RPT, RS4>(Xs, rg, g, hv);
@@ -936,8 +939,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         for (int j = 0; j < 8; ++j) {
           const int u = unit_of<W>(g, j);
           if constexpr (JET) {
-            const T s = stash[st_idx(0, j * NST0)];
-            const T c = C::SIN ? stash[st_idx(0, j * NST0 + 1)] : T(0);
+            const T s = st_at(0)[(j * NST0) * NT];
+            const T c = C::SIN ? st_at(0)[(j * NST0 + 1) * NT] : T(0);
             T d1, d2;
             act_d12<ACT>(s, c, d1, d2);
             const T d3 = act_d3<ACT>(s, c, d1, d2);
@@ -964,8 +967,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           } else {
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-              const T s = stash[st_idx(0, (r * 8 + j) * NST0)];
-              const T c = C::SIN ? stash[st_idx(0, (r * 8 + j) * NST0 + 1)] : T(0);
+              const T s = st_at(0)[((r * 8 + j) * NST0) * NT];
+              const T c = C::SIN ? st_at(0)[((r * 8 + j) * NST0 + 1) * NT] : T(0);
               T d1, d2;
               act_d12<ACT>(s, c, d1, d2);
               zb[r][j] = sb[r][j] * d1;
