@@ -43,7 +43,7 @@ enum { FR_ACT_TANH = 0, FR_ACT_SIN = 1 };                                /* _ker
 enum { FR_STEADY2D = 0, FR_UNSTEADY2D = 1, FR_UNSTEADY3D = 2 };          /* physics._KINDS */
 enum { FR_F32 = 0, FR_F64 = 1 };
 enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3 };
-enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2 };
+enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2, FR_FLAG_EXCHANGE_TIMEOUT = 4 };
 /* contraction math of the training kernels: FP32 SIMT (oracle parity ~1e-5) or
  * TF32 tcgen05 tensor cores (wide FP32 experts, 64 < width <= 512; default) */
 enum { FR_MATH_SIMT = 0, FR_MATH_TF32 = 1 };
@@ -114,6 +114,36 @@ int fr_epoch_workspace(const fr_plan* plan, long long n_colloc, const long long*
 int fr_epoch_fwd_bwd(const fr_plan* plan, const void* kparams, const void* colloc, long long n_colloc,
                      double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
                      double* gpart, double* const* lpart_blocks, void* scratch, fr_stream_t stream);
+
+/* Ghost-exchange overlap (worker.py:170-228 / driver.py:133-142).
+ * The epoch launch starts before this rank's ghost targets have arrived: the
+ * MSE sets from `first_gated_set` on (the ghost sets; obs is never gated) wait
+ * inside the kernel until *gate != 0, which the transport stream sets with
+ * fr_signal() once the NCCL receives (or in-process copies) have landed.  Each
+ * CTA reaches its ghost tiles only after all of its PDE and obs tiles, so the
+ * exchange latency hides under the interior work.  max_ctas caps the persistent
+ * grid so the transport's kernels keep free SMs (0 = every SM); the workspace
+ * must be sized with the same cap (fr_epoch_workspace_capped).  A wait longer
+ * than timeout_ms or-s FR_FLAG_EXCHANGE_TIMEOUT into *flags and proceeds (the
+ * host raises; drop-in for the reference's DeadlockError, driver.py:161-166). */
+typedef struct {
+  const unsigned* gate;
+  int first_gated_set;
+  int max_ctas;
+  int* flags;
+  unsigned timeout_ms;
+} fr_epoch_gate;
+
+int fr_epoch_workspace_capped(const fr_plan* plan, long long n_colloc, const long long* n_sets, int n_set_count,
+                              int max_ctas, fr_workspace* out);
+int fr_epoch_fwd_bwd_gated(const fr_plan* plan, const void* kparams, const void* colloc, long long n_colloc,
+                           double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
+                           double* gpart, double* const* lpart_blocks, void* scratch, const fr_epoch_gate* gate,
+                           fr_stream_t stream);
+/* *word = value once every prior operation on `stream` has completed (one
+ * single-thread kernel, release ordering); with delay_ns > 0 it first sleeps
+ * that long on the device (tests emulate a slow transport with it) */
+int fr_signal(unsigned* word, unsigned value, unsigned delay_ns, fr_stream_t stream);
 
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,

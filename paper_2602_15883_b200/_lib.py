@@ -16,7 +16,7 @@ ACT_TANH, ACT_SIN = 0, 1
 STEADY2D, UNSTEADY2D, UNSTEADY3D = 0, 1, 2
 F32, F64 = 0, 1
 MODE_PDE, MODE_MSE, MODE_VALUE, MODE_JET = 0, 1, 2, 3
-FLAG_NONFINITE_LOSS, FLAG_NONFINITE_GRAD = 1, 2
+FLAG_NONFINITE_LOSS, FLAG_NONFINITE_GRAD, FLAG_EXCHANGE_TIMEOUT = 1, 2, 4
 
 REGIME_CODES = {"steady2d": STEADY2D, "unsteady2d": UNSTEADY2D, "unsteady3d": UNSTEADY3D}
 ACT_CODES = {"tanh": ACT_TANH, "sin": ACT_SIN}
@@ -63,6 +63,11 @@ class AdamArgs(C.Structure):
     ]
 
 
+class EpochGate(C.Structure):
+    _fields_ = [("gate", C.c_void_p), ("first_gated_set", C.c_int), ("max_ctas", C.c_int),
+                ("flags", C.c_void_p), ("timeout_ms", C.c_uint)]
+
+
 class MseSet(C.Structure):
     _fields_ = [("pts", C.c_void_p), ("target_u", C.c_void_p), ("target_p", C.c_void_p),
                 ("n", C.c_longlong), ("vel_coef", C.c_double), ("p_coef", C.c_double)]
@@ -82,6 +87,11 @@ _SIGS = {
     "fr_epoch_workspace": [_P, C.c_longlong, C.POINTER(C.c_longlong), C.c_int, C.POINTER(Workspace)],
     "fr_epoch_fwd_bwd": [_P, _P, _P, C.c_longlong, C.c_double, C.POINTER(MseSet), C.c_int, _P, _P,
                          C.POINTER(C.c_void_p), _P, _P],
+    "fr_epoch_workspace_capped": [_P, C.c_longlong, C.POINTER(C.c_longlong), C.c_int, C.c_int,
+                                  C.POINTER(Workspace)],
+    "fr_epoch_fwd_bwd_gated": [_P, _P, _P, C.c_longlong, C.c_double, C.POINTER(MseSet), C.c_int, _P, _P,
+                               C.POINTER(C.c_void_p), _P, C.POINTER(EpochGate), _P],
+    "fr_signal": [_P, C.c_uint, C.c_uint, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
@@ -127,7 +137,8 @@ def lib():
 
 # functions that enqueue kernels (counted for the bench's gpu_launches claim)
 LAUNCHERS = frozenset({
-    "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
+    "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_epoch_fwd_bwd_gated",
+    "fr_signal", "fr_value_fwd", "fr_jet_fwd",
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_jet_act_forward",
     "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
 })

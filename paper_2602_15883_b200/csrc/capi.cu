@@ -469,11 +469,17 @@ static int epoch_info(const fr_plan* p, KInfo* ki) {
 
 extern "C" int fr_epoch_workspace(const fr_plan* p, long long n_colloc, const long long* n_sets, int n_set_count,
                                   fr_workspace* out) {
-  if (!p || !out || n_set_count < 0 || n_set_count > 3 || (n_set_count && !n_sets))
+  return fr_epoch_workspace_capped(p, n_colloc, n_sets, n_set_count, 0, out);
+}
+
+extern "C" int fr_epoch_workspace_capped(const fr_plan* p, long long n_colloc, const long long* n_sets,
+                                         int n_set_count, int max_ctas, fr_workspace* out) {
+  if (!p || !out || n_set_count < 0 || n_set_count > 3 || (n_set_count && !n_sets) || max_ctas < 0)
     return fail("fr_epoch_workspace: bad arguments");
   KInfo ki{};
   if (epoch_info(p, &ki)) return 1;
-  const int sms = p->info.num_sms > 0 ? p->info.num_sms : 148;
+  int sms = p->info.num_sms > 0 ? p->info.num_sms : 148;
+  if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
   long long tiles = (n_colloc + ki.ppt - 1) / ki.ppt;
   for (int i = 0; i < n_set_count; ++i) tiles += (n_sets[i] + ki.ppt_mse - 1) / ki.ppt_mse;
   out->grid = int(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
@@ -490,9 +496,20 @@ extern "C" int fr_epoch_workspace(const fr_plan* p, long long n_colloc, const lo
 extern "C" int fr_epoch_fwd_bwd(const fr_plan* p, const void* kparams, const void* colloc, long long n_colloc,
                                 double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
                                 double* gpart, double* const* lpart_blocks, void* scratch, fr_stream_t stream) {
+  return fr_epoch_fwd_bwd_gated(p, kparams, colloc, n_colloc, pde_coef, sets, n_set_count, vel_w, gpart,
+                                lpart_blocks, scratch, nullptr, stream);
+}
+
+extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, const void* colloc, long long n_colloc,
+                                      double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
+                                      double* gpart, double* const* lpart_blocks, void* scratch,
+                                      const fr_epoch_gate* gate, fr_stream_t stream) {
   if (!p || !kparams || !colloc || n_colloc < 1 || !gpart || !lpart_blocks || !scratch || n_set_count < 0 ||
       n_set_count > 3 || (n_set_count && !sets))
     return fail("fr_epoch_fwd_bwd: bad arguments");
+  if (gate && (!gate->gate || gate->first_gated_set < 0 || gate->max_ctas < 0))
+    return fail("fr_epoch_fwd_bwd_gated: bad gate");
+  if (gate && p->info.width_pad > 64) return fail("fr_epoch_fwd_bwd_gated: fused epoch path only (width <= 64)");
   long long ns[3] = {0, 0, 0};
   for (int i = 0; i < n_set_count; ++i) {
     if (sets[i].n < 0 || (sets[i].n > 0 && (!sets[i].pts || !sets[i].target_u)))
@@ -502,7 +519,7 @@ extern "C" int fr_epoch_fwd_bwd(const fr_plan* p, const void* kparams, const voi
   for (int i = 0; i < 1 + n_set_count; ++i)
     if (!lpart_blocks[i]) return fail("fr_epoch_fwd_bwd: NULL loss-partial block %d", i);
   fr_workspace ws;
-  if (fr_epoch_workspace(p, n_colloc, ns, n_set_count, &ws)) return 1;
+  if (fr_epoch_workspace_capped(p, n_colloc, ns, n_set_count, gate ? gate->max_ctas : 0, &ws)) return 1;
   KInfo ki{};
   if (epoch_info(p, &ki)) return 1;
   const fr_plan_info& I = p->info;
@@ -534,8 +551,34 @@ extern "C" int fr_epoch_fwd_bwd(const fr_plan* p, const void* kparams, const voi
     e.mse[i].coef = sets[i].vel_coef;
     e.mse[i].pcoef = sets[i].p_coef;
     e.mse[i].lpart = lpart_blocks[1 + i];
+    if (gate && i >= gate->first_gated_set) {
+      e.mse[i].gate = gate->gate;
+      e.mse[i].flags = gate->flags;
+      e.mse[i].gate_timeout_ns = (unsigned long long)(gate->timeout_ms ? gate->timeout_ms : 60000u) * 1000000ull;
+    }
   }
   return epoch_call(p, &e, ws.grid, stream, nullptr);
+}
+
+__global__ void signal_kernel(unsigned* word, unsigned value, unsigned delay_ns) {
+  if (delay_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      __nanosleep(1000);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < delay_ns);
+  }
+  __threadfence_system();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(word), "r"(value) : "memory");
+}
+
+extern "C" int fr_signal(unsigned* word, unsigned value, unsigned delay_ns, fr_stream_t stream) {
+  if (!word) return fail("fr_signal: NULL word");
+  signal_kernel<<<1, 1, 0, stream>>>(word, value, delay_ns);
+  ++g_kernel_launches;
+  FR_CUDA(cudaGetLastError(), "fr_signal");
+  return 0;
 }
 
 extern "C" int fr_value_fwd(const fr_plan* p, const void* kparams, const void* pts, long long n, void* out,

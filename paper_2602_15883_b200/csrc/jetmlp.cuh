@@ -67,6 +67,8 @@ template <int MODE, int REG> struct Streams {
   static constexpr int RPT = JET ? S : 6;
 };
 
+constexpr int FLAG_EXCHANGE_TIMEOUT = 4;  // == FR_FLAG_EXCHANGE_TIMEOUT (flowrec_b200.h)
+
 struct KArgs {
   const void* kp;       // kernel params (T), padded layout, see ParamLayout
   const void* pts;      // (n, DIN) T
@@ -85,6 +87,9 @@ struct KArgs {
   double inv_re;        // PDE: 1/Re (physics.py:80)
   double velw[4];       // MSE: velocity component weights
   int has_p;            // MSE: pressure head present
+  const unsigned* gate; // MSE: wait until *gate != 0 before the first tile (ghost overlap)
+  int* flags;           // FLAG_EXCHANGE_TIMEOUT on a timed-out gate wait
+  unsigned long long gate_timeout_ns;
 };
 
 // Padded flat parameter layout used by the kernels (T precision):

@@ -186,6 +186,25 @@ struct JetCfg {
   }
 };
 
+// Ghost-overlap gate (fr_epoch_gate): spin with back-off until the transport
+// stream has published this rank's ghost targets; bounded, so a lost peer
+// becomes a flagged error instead of a hung GPU.
+static __device__ __noinline__ void gate_wait(const unsigned* gate, int* flags, unsigned long long timeout_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+    if (v != 0u) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      if (flags) atomicOr(flags, FLAG_EXCHANGE_TIMEOUT);
+      return;
+    }
+    __nanosleep(1000);
+  }
+}
+
 // element (row, k) of a k-quad buffer
 template <int RS4>
 __device__ __forceinline__ int kqi(int row, int k) {
@@ -205,6 +224,16 @@ __device__ __forceinline__ int unit_of(int g, int j) {
 // operations to one location stay in program order, so the result is the
 // same fixed-order sum on every run.
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
+
+// FP32 inner-loop unroll factors (tuned on B200; overridable for sweeps)
+#ifndef FR_GEMM_UNROLL
+#define FR_GEMM_UNROLL 8
+#endif
+#ifndef FR_DW_UNROLL
+#define FR_DW_UNROLL 4
+#endif
+constexpr int kGemmUnroll = FR_GEMM_UNROLL;
+constexpr int kDwUnroll = FR_DW_UNROLL;
 
 // ---------------------------------------------------------------------------
 // packed FP32 pairs (sm_100a FFMA2: fma.rn.f32x2, one issue slot for two FMAs).
@@ -246,7 +275,7 @@ __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __re
       for (int q = 0; q < 4; ++q) acc2[r][q] = 0ull;
     const float* ap = reinterpret_cast<const float*>(A) + rg * (4 * RPT);
     const float* bp = reinterpret_cast<const float*>(B) + 4 * g;
-#pragma unroll 8
+#pragma unroll kGemmUnroll
     for (int kq = 0; kq < W / 4; ++kq) {
       float av[4 * RPT];
       vload(av, ap + kq * RS4);
@@ -416,6 +445,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   __syncthreads();
 
   const long long ntiles = (n + PPT - 1) / PPT;
+  if constexpr (MODE == MODE_MSE) {
+    if (a.gate != nullptr && t0 < ntiles) {
+      if (tid == 0) gate_wait(a.gate, a.flags, a.gate_timeout_ns);
+      __syncthreads();
+    }
+  }
 #ifdef FR_PHASE_TIMERS
   long long ph_acc[16] = {0};
   long long ph_last = clock64();
@@ -427,11 +462,12 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       const long long rem = n - p0;
       for (int i = tid; i < PPT * DIN; i += NT) Ps[i] = (i / DIN < rem) ? pts[i] : T(0);
       if constexpr (MODE == MODE_MSE) {
+        // L2-coherent loads: ghost targets may land while this kernel runs (gate)
         const T* tu = static_cast<const T*>(a.tu) + p0 * NVEL;
-        for (int i = tid; i < PPT * NVEL; i += NT) TUs[i] = (i / NVEL < rem) ? tu[i] : T(0);
+        for (int i = tid; i < PPT * NVEL; i += NT) TUs[i] = (i / NVEL < rem) ? __ldcg(tu + i) : T(0);
         if (a.has_p) {
           const T* tpp = static_cast<const T*>(a.tp) + p0;
-          for (int i = tid; i < PPT; i += NT) TPs[i] = (i < rem) ? tpp[i] : T(0);
+          for (int i = tid; i < PPT; i += NT) TPs[i] = (i < rem) ? __ldcg(tpp + i) : T(0);
         }
       }
     }
@@ -833,7 +869,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
               for (int x = 0; x < 8; ++x)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc2[x][q] = 0ull;
-#pragma unroll 4
+#pragma unroll kDwUnroll
               for (int r = 0; r < RROWS; ++r) {
                 float h[8];
                 f32x2 z[4];

@@ -20,6 +20,7 @@ parameters after epoch e-1, including e = 0 (:133-142); history rows are the
 pre-update unweighted parts; masters normalise every outgoing pressure.
 """
 
+import ctypes as C
 import os
 import time
 from dataclasses import dataclass
@@ -27,14 +28,11 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .. import _lib as X
 from ..decomposition import identify_masters
 from ..network import ExpertConfig, ExpertParams
 from ..physics import FlowRegime
-from .worker import OutgoingEdge, RankWorker, TrainConfig, WorkerSpec, derive_param_seed
-
-
-class DeadlockError(RuntimeError):
-    pass
+from .worker import DeadlockError, OutgoingEdge, RankWorker, TrainConfig, WorkerSpec, derive_param_seed
 
 
 class RankFailure(RuntimeError):
@@ -99,13 +97,37 @@ def build_plan(subdomains, datasets, expert_config: ExpertConfig, train_config: 
 # -- in-process (single GPU, all ranks) ---------------------------------------------
 
 
-class LocalTrainer:
-    """All ranks of a plan resident on one GPU with a device-to-device exchange."""
+def _overlap_max_ctas(reserve_sms):
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return max(1, sms - int(reserve_sms))
 
-    def __init__(self, plan: TrainingPlan, dtype="float32", epochs=None):
+
+class LocalTrainer:
+    """All ranks of a plan resident on one GPU with a device-to-device exchange.
+
+    overlap=True runs the exchange the way the one-process-per-GPU trainer
+    does: the packs into the destinations' target rows go on a transport
+    stream that publishes each rank's gate word, and the epoch kernels start
+    at once, their ghost heads waiting in-kernel (fr_epoch_fwd_bwd_gated).
+    `signal_delay_ns` holds every gate back that long (tests use it to prove
+    the in-kernel wait, not stream order, protects the ghost heads)."""
+
+    def __init__(self, plan: TrainingPlan, dtype="float32", epochs=None, overlap=False, reserve_sms=None,
+                 signal_delay_ns=0):
         self.plan = plan
-        self.workers = {ws.rank: RankWorker(ws, dtype=dtype, epochs=epochs) for ws in plan.worker_specs}
+        self.overlap = bool(overlap)
+        self.signal_delay_ns = int(signal_delay_ns)
+        if reserve_sms is None:
+            reserve_sms = 2 if self.overlap else 0
+        max_ctas = _overlap_max_ctas(reserve_sms) if reserve_sms else 0
+        self.workers = {ws.rank: RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas)
+                        for ws in plan.worker_specs}
         self.order = sorted(self.workers)
+        if self.overlap:
+            self.comm = torch.cuda.Stream()
+            self.gates = torch.zeros(len(self.order), dtype=torch.int32, device="cuda")
+            self.gate_args = {r: self.workers[r].objective.make_gate(self.gates[i], self.workers[r].flags)
+                              for i, r in enumerate(self.order)}
         self.routes = []
         for r in self.order:
             w = self.workers[r]
@@ -128,9 +150,30 @@ class LocalTrainer:
             self.workers[r].enqueue_epoch()
 
     def _enqueue(self, exchange):
+        if exchange and self.overlap:
+            self._enqueue_overlapped()
+            return
         if exchange:
             self.enqueue_exchange()
         self.enqueue_step()
+
+    def _enqueue_overlapped(self):
+        for r in self.order:
+            self.workers[r].produce()
+        self.gates.zero_()
+        cur = torch.cuda.current_stream()
+        self.comm.wait_stream(cur)
+        with torch.cuda.stream(self.comm):
+            for w, k, tu, tp in self.routes:
+                w.pack_edge(k, tu, tp, stream=self.comm)
+            for i, r in enumerate(self.order):
+                X.call("fr_signal", C.c_void_p(self.gates[i].data_ptr()), 1, self.signal_delay_ns,
+                       X.stream_ptr(self.comm))
+        for w in self.workers.values():
+            w.objective.mark_targets_set()
+        for r in self.order:
+            self.workers[r].enqueue_epoch(gate=self.gate_args[r] if self.workers[r].objective.ghost else None)
+        cur.wait_stream(self.comm)
 
     def _graph(self, exchange):
         g = self.graphs.get(exchange)
@@ -222,37 +265,69 @@ def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
 
 
 class DistributedTrainer:
-    """This process's rank of a torch.distributed group (NCCL over NVLink)."""
+    """This process's rank of a torch.distributed group (NCCL over NVLink).
 
-    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None):
+    overlap=True (default for the fused small-width kernel): the ghost
+    exchange is overlapped with the interior work.  The producer and pack run
+    on the compute stream; the NCCL send/recv group then runs on a transport
+    stream which, once the receives have landed, sets this rank's gate word
+    (fr_signal).  The epoch kernel is launched immediately with its persistent
+    grid capped `reserve_sms` below the SM count (so NCCL's kernels have SMs to
+    run on); every CTA walks its PDE and observation tiles first and only its
+    ghost tiles wait on the gate, so the transfer hides under the interior
+    residual work.  The first exchange runs in stream order (it also brings up
+    the NCCL connections, which may synchronise the device)."""
+
+    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=2):
         import torch.distributed as dist
 
         self.plan = plan
         self.rank = dist.get_rank() if rank is None else rank
         if dist.get_world_size() != plan.n_ranks:
             raise ValueError(f"world size {dist.get_world_size()} != plan ranks {plan.n_ranks}")
-        self.worker = w = RankWorker(plan.worker_specs[self.rank], dtype=dtype, epochs=epochs)
+        ws = plan.worker_specs[self.rank]
+        wide = max(plan.expert_config.arch[1:-1], default=0) > 64
+        self.overlap = bool(overlap) and not wide and len(ws.datasets.ghosts) > 0
+        max_ctas = _overlap_max_ctas(reserve_sms) if self.overlap else 0
+        self.worker = w = RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas)
         self.sends, self.recvs = p2p_routes(plan, self.rank)
         nv, T, dev = plan.regime.n_vel, w.plan.tdtype, w.plan.device
         self.send_bufs = [(torch.empty((n, nv), dtype=T, device=dev), torch.empty(n, dtype=T, device=dev))
                           for _, _, n in self.sends]
         self.recv_bufs = {gi: w.objective.target_slice(gi) for _, gi, _ in self.recvs}
+        self._connected = False
+        if self.overlap:
+            self.comm = torch.cuda.Stream()
+            self.gate_word = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.gate = w.objective.make_gate(self.gate_word, w.flags)
 
     def epoch(self, e):
-        """Exchange (if due) then the fused epoch.  The persistent epoch kernel
-        occupies every SM, so NCCL's P2P kernels could not run underneath it;
-        the (latency-bound, ~10-30 us) exchange is therefore issued first and
-        the epoch kernel consumes the received ghost targets directly."""
+        """Exchange (if due) then the fused epoch (overlapped, see the class doc)."""
         w = self.worker
         exchange = e % self.plan.train_config.comm_interval == 0
+        gate = None
         if exchange:
             w.produce()
             for k, _ in enumerate(self.sends):
                 w.pack_edge(k, *self.send_bufs[k])
-            for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
-                wk.wait()  # orders the compute stream after the transfers (no host sync)
+            if self.overlap and self._connected:
+                cur = torch.cuda.current_stream()
+                self.gate_word.zero_()
+                self.comm.wait_stream(cur)
+                with torch.cuda.stream(self.comm):
+                    for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                        wk.wait()  # transport stream waits for the transfers
+                    X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
+                gate = self.gate
+            else:
+                for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                    wk.wait()  # orders the compute stream after the transfers (no host sync)
+                self._connected = True
             w.objective.mark_targets_set()
-        w.enqueue_epoch()
+        w.enqueue_epoch(gate=gate)
+        if gate is not None:
+            # send buffers / targets are reused by the next round
+            torch.cuda.current_stream().wait_stream(self.comm)
         w.epochs_done += 1
         if exchange:
             w.exchange_log.append((e, sorted(w.expected_messages)))

@@ -29,8 +29,9 @@ KINDS = ("spatial", "temporal")
 class DeviceObjective:
     """Resident datasets, workspaces and the per-epoch launch sequence."""
 
-    def __init__(self, plan, regime, datasets, weights):
+    def __init__(self, plan, regime, datasets, weights, max_ctas=0):
         self.plan = plan
+        self.max_ctas = int(max_ctas)  # persistent-grid cap (SMs left free for the exchange transport)
         self.regime = regime
         self.weights = weights
         dev, T = plan.device, plan.tdtype
@@ -90,7 +91,8 @@ class DeviceObjective:
             return
         n_sets = (ctypes.c_longlong * 3)(*([self._set_n(sg, k) for sg, k in self.set_order] + [0] * 3)[:3])
         ws = X.Workspace()
-        X.call("fr_epoch_workspace", plan.h, self.n_colloc, n_sets, len(self.set_order), ctypes.byref(ws))
+        X.call("fr_epoch_workspace_capped", plan.h, self.n_colloc, n_sets, len(self.set_order), self.max_ctas,
+               ctypes.byref(ws))
         self.ws = ws
         self.grid = ws.grid
         present = [SEG_OBS] if self.n_obs else []
@@ -116,6 +118,15 @@ class DeviceObjective:
         self.grad = torch.zeros(plan.info.n_params, dtype=torch.float64, device=dev)
         self.norm_parts = torch.zeros(X.lib().fr_reduce_grad_parts(plan.h), dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+        # ghost sets follow obs in set_order: the overlapped exchange gates them
+        self.first_ghost_set = 1 if self.n_obs else 0
+
+    def make_gate(self, gate_word, flags, timeout_ms=60000):
+        """fr_epoch_gate for the overlapped exchange (ghost sets wait on gate_word)."""
+        if self.wide:
+            raise ValueError("the overlapped exchange needs the fused epoch kernel (hidden width <= 64)")
+        return X.EpochGate(gate_word.data_ptr(), self.first_ghost_set, self.max_ctas, flags.data_ptr(),
+                           int(timeout_ms))
 
     def _init_wide(self, plan, counts, weights, dev):
         """Wide experts (hidden width > 64): one layer-wise launch sequence per
@@ -198,10 +209,12 @@ class DeviceObjective:
                     n_ghost_time=float(self.n_ghost["temporal"]), w_obs=w.obs, w_pde=w.pde,
                     w_ghost_u=w.ghost_u, w_ghost_p_space=w.ghost_p_space, w_ghost_p_time=w.ghost_p_time)
 
-    def enqueue(self, kparams, stream=None, with_sums=True):
+    def enqueue(self, kparams, stream=None, with_sums=True, gate=None):
         """Launch the epoch's loss/gradient kernel and the fixed-order gradient
         reduction (no sync).  with_sums also reduces the loss partials into
-        `sums` (the training loop leaves that to the optimiser kernel)."""
+        `sums` (the training loop leaves that to the optimiser kernel).  With a
+        `gate` (make_gate) the ghost heads wait inside the kernel for the
+        exchange instead of the launch waiting for it."""
         for kind in self.ghost:
             if not self.targets_set[kind]:
                 raise RuntimeError(f"{kind} ghost targets were never set; run an exchange first")
@@ -210,9 +223,10 @@ class DeviceObjective:
         if self.wide:
             self._enqueue_wide(kparams, st)
         else:
-            X.call("fr_epoch_fwd_bwd", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
+            X.call("fr_epoch_fwd_bwd_gated", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
                    self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
-                   X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch), st)
+                   X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch),
+                   ctypes.byref(gate) if gate is not None else None, st)
         X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
                X.ptr(self.norm_parts), st)
         if with_sums:
