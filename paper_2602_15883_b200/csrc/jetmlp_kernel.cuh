@@ -356,6 +356,74 @@ __device__ __forceinline__ void load_block(T (&v)[RPT][8], const T* __restrict__
 }
 
 // ---------------------------------------------------------------------------
+// per-CTA activation stash (L2-resident).  Element q of thread t of a layer
+// region lives at quad (q >> 2): [(q >> 2) * 4 * NT + 4 * t + (q & 3)], so a
+// thread's consecutive elements share 16-byte quads and runs of them move as
+// STG.128 / STG.64 (LDG likewise) while each warp access stays coalesced.
+// `lb` below is the layer base already offset by 4 * t.
+// ---------------------------------------------------------------------------
+template <int NT, typename T>
+__device__ __forceinline__ T& sq(T* lb, int q) {
+  return lb[(q >> 2) * (4 * NT) + (q & 3)];
+}
+template <typename T>
+__device__ __forceinline__ void vst2(T* p, T a, T b) {
+  if constexpr (sizeof(T) == 4) *reinterpret_cast<float2*>(p) = make_float2(a, b);
+  else *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+template <typename T>
+__device__ __forceinline__ void vld2(const T* p, T& a, T& b) {
+  if constexpr (sizeof(T) == 4) { const float2 v = *reinterpret_cast<const float2*>(p); a = v.x; b = v.y; }
+  else { const double2 v = *reinterpret_cast<const double2*>(p); a = v.x; b = v.y; }
+}
+// v[0..N) -> elements q0..q0+N-1 (q0 is a compile-time constant after unrolling,
+// so every branch below folds)
+template <int NT, int N, typename T>
+__device__ __forceinline__ void st_run(T* lb, int q0, const T (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i + 1 < N; i += 2) {
+    const int q = q0 + i;
+    T* p = &sq<NT>(lb, q);
+    if ((q & 3) == 0 && i + 4 <= N) {
+      if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(p) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      else { vst2(p, v[i], v[i + 1]); vst2(p + 2, v[i + 2], v[i + 3]); }
+    } else if ((q & 3) == 2 && i >= 2 && i + 2 <= N) {
+      // second half of the quad stored at i - 2
+    } else if ((q & 1) == 0) {
+      vst2(p, v[i], v[i + 1]);
+    } else {
+      *p = v[i];
+      sq<NT>(lb, q + 1) = v[i + 1];
+    }
+  }
+  if constexpr (N & 1) sq<NT>(lb, q0 + N - 1) = v[N - 1];
+}
+template <int NT, int N, typename T>
+__device__ __forceinline__ void ld_run(T (&v)[N], const T* lb, int q0) {
+#pragma unroll
+  for (int i = 0; i + 1 < N; i += 2) {
+    const int q = q0 + i;
+    const T* p = &sq<NT>(const_cast<T*>(lb), q);
+    if ((q & 3) == 0 && i + 4 <= N) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(p);
+        v[i] = x.x; v[i + 1] = x.y; v[i + 2] = x.z; v[i + 3] = x.w;
+      } else {
+        vld2(p, v[i], v[i + 1]);
+        vld2(p + 2, v[i + 2], v[i + 3]);
+      }
+    } else if ((q & 3) == 2 && i >= 2 && i + 2 <= N) {
+    } else if ((q & 1) == 0) {
+      vld2(p, v[i], v[i + 1]);
+    } else {
+      v[i] = *p;
+      v[i + 1] = sq<NT>(const_cast<T*>(lb), q + 1);
+    }
+  }
+  if constexpr (N & 1) v[N - 1] = sq<NT>(const_cast<T*>(lb), q0 + N - 1);
+}
+
+// ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 // Processes tiles t0, t0 + tstride, ... of one dataset with this CTA.  Gradient
@@ -415,9 +483,9 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       for (int i = tid; i < a.np_pad; i += NT) gp[i] = 0.0;
   }
   T* stash = static_cast<T*>(a.scratch) + size_t(blockIdx.x) * a.stash_elems;
-  // stash element q of `layer` for this thread lives at st_at(layer)[q * NT]:
-  // one 64-bit base per layer, every q an immediate offset (coalesced over tid)
-  T* const stash_t = stash + tid;
+  // stash element q of `layer` for this thread: sq<NT>(st_at(layer), q) -- one
+  // 64-bit base per layer, every q an immediate offset (quad layout above)
+  T* const stash_t = stash + 4 * tid;
   auto st_at = [&](int layer) { return stash_t + size_t(C::stash_layer_base(layer)) * NT; };
 
   double lacc0 = 0.0, lacc1 = 0.0;
@@ -477,6 +545,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
     // ---------------- layer 0 (DIN -> W): derivative blocks are constant ----------------
     {
       T outv[RPT][8];
+      T s0v[8 * NST0];  // JET: layer-0 stash run (s, [c]) over this thread's 8 units
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int u = unit_of<W>(g, j);
@@ -505,11 +574,17 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             outv[pr][j] = s;
           }
           if constexpr (BWD) {
-            st_at(0)[((pr * 8 + j) * NST0) * NT] = s;
-            if constexpr (C::SIN) st_at(0)[((pr * 8 + j) * NST0 + 1) * NT] = c;
+            if constexpr (JET) {
+              s0v[j * NST0] = s;
+              if constexpr (C::SIN) s0v[j * NST0 + 1] = c;
+            } else {
+              sq<NT>(st_at(0), ((pr * 8 + j) * NST0)) = s;
+              if constexpr (C::SIN) sq<NT>(st_at(0), ((pr * 8 + j) * NST0 + 1)) = c;
+            }
           }
         }
       }
+      if constexpr (BWD && JET) st_run<NT>(st_at(0), 0, s0v);
       store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
     }
     __syncthreads();
@@ -542,18 +617,21 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             outv[1 + NG + i][j] = d2 * zg * zg + d1 * acc[1 + NG + i][j];
           }
           if constexpr (BWD) {
-            const int q = j * NSTH;
+            // one run of 2S: the S output streams, then the S adjoint factors
+            static_assert(NSTH == 2 * S && 1 + NG + NL == S, "jet stash run layout");
             const T d3 = act_d3<ACT>(s, c, d1, d2);
+            T sv[2 * S];
 #pragma unroll
-            for (int st = 0; st < S; ++st) st_at(l)[(q + st) * NT] = outv[st][j];
-            st_at(l)[(q + S) * NT] = d1;
+            for (int st = 0; st < S; ++st) sv[st] = outv[st][j];
+            sv[S] = d1;
 #pragma unroll
-            for (int i = 0; i < NG; ++i) st_at(l)[(q + S + 1 + i) * NT] = d2 * acc[1 + i][j];
+            for (int i = 0; i < NG; ++i) sv[S + 1 + i] = d2 * acc[1 + i][j];
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
               const T zg = acc[1 + LAP0 + i][j];
-              st_at(l)[(q + S + 1 + NG + i) * NT] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
+              sv[S + 1 + NG + i] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
             }
+            st_run<NT>(st_at(l), j * NSTH, sv);
           }
         } else {
 #pragma unroll
@@ -563,8 +641,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             act_eval<ACT>(zv, s, c);
             outv[r][j] = s;
             if constexpr (BWD) {
-              st_at(l)[((r * 8 + j) * NST0) * NT] = s;
-              if constexpr (C::SIN) st_at(l)[((r * 8 + j) * NST0 + 1) * NT] = c;
+              sq<NT>(st_at(l), ((r * 8 + j) * NST0)) = s;
+              if constexpr (C::SIN) sq<NT>(st_at(l), ((r * 8 + j) * NST0 + 1)) = c;
             }
           }
         }
@@ -773,13 +851,14 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           for (int j = 0; j < 8; ++j) {
             if constexpr (JET) {
               // numpy_backend.py:58-89 with the forward-time factors
-              const int q = j * NSTH + S;
-              const T d1 = st_at(l)[(q) * NT];
+              T fv[S];
+              ld_run<NT>(fv, st_at(l), j * NSTH + S);
+              const T d1 = fv[0];
               T ga[NG], lb[NL > 0 ? NL : 1];
 #pragma unroll
-              for (int i = 0; i < NG; ++i) ga[i] = st_at(l)[(q + 1 + i) * NT];
+              for (int i = 0; i < NG; ++i) ga[i] = fv[1 + i];
 #pragma unroll
-              for (int i = 0; i < NL; ++i) lb[i] = st_at(l)[(q + 1 + NG + i) * NT];
+              for (int i = 0; i < NL; ++i) lb[i] = fv[1 + NG + i];
               T zv = sb[0][j] * d1;
 #pragma unroll
               for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * ga[i];
@@ -797,8 +876,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             } else {
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
-                const T s = st_at(l)[((r * 8 + j) * NST0) * NT];
-                const T c = C::SIN ? st_at(l)[((r * 8 + j) * NST0 + 1) * NT] : T(0);
+                const T s = sq<NT>(st_at(l), ((r * 8 + j) * NST0));
+                const T c = C::SIN ? sq<NT>(st_at(l), ((r * 8 + j) * NST0 + 1)) : T(0);
                 T d1, d2;
                 act_d12<ACT>(s, c, d1, d2);
                 zb[r][j] = sb[r][j] * d1;
@@ -811,13 +890,17 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         {
           T hv[RPT][8];
           const int lp = l - 1;
+          T s0v[8 * NST0];
+          if constexpr (JET) {
+            if (lp == 0) ld_run<NT>(s0v, st_at(0), 0);
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int u = unit_of<W>(g, j);
             if constexpr (JET) {
               if (lp == 0) {
-                const T s = st_at(0)[(j * NST0) * NT];
-                const T c = C::SIN ? st_at(0)[(j * NST0 + 1) * NT] : T(0);
+                const T s = s0v[j * NST0];
+                const T c = C::SIN ? s0v[j * NST0 + 1] : T(0);
                 T d1, d2;
                 act_d12<ACT>(s, c, d1, d2);
                 hv[0][j] = s;
@@ -830,11 +913,16 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                 }
               } else {
 #pragma unroll
-                for (int st = 0; st < S; ++st) hv[st][j] = st_at(lp)[(j * NSTH + st) * NT];
+                {
+                  T hvv[S];
+                  ld_run<NT>(hvv, st_at(lp), j * NSTH);
+#pragma unroll
+                  for (int st = 0; st < S; ++st) hv[st][j] = hvv[st];
+                }
               }
             } else {
 #pragma unroll
-              for (int r = 0; r < RPT; ++r) hv[r][j] = st_at(lp)[((r * 8 + j) * NST0) * NT];
+              for (int r = 0; r < RPT; ++r) hv[r][j] = sq<NT>(st_at(lp), ((r * 8 + j) * NST0));
             }
           }
           store_block<T, W, RPT, RS4>(Xs, rg, g, hv);
@@ -971,12 +1059,14 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         T sb[RPT][8];
         load_block<T, W, RPT, RS4>(sb, Gs, rg, g);
         T zb[RPT][8];
+        T s0v[8 * NST0];
+        if constexpr (JET) ld_run<NT>(s0v, st_at(0), 0);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int u = unit_of<W>(g, j);
           if constexpr (JET) {
-            const T s = st_at(0)[(j * NST0) * NT];
-            const T c = C::SIN ? st_at(0)[(j * NST0 + 1) * NT] : T(0);
+            const T s = s0v[j * NST0];
+            const T c = C::SIN ? s0v[j * NST0 + 1] : T(0);
             T d1, d2;
             act_d12<ACT>(s, c, d1, d2);
             const T d3 = act_d3<ACT>(s, c, d1, d2);
@@ -1003,8 +1093,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           } else {
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-              const T s = st_at(0)[((r * 8 + j) * NST0) * NT];
-              const T c = C::SIN ? st_at(0)[((r * 8 + j) * NST0 + 1) * NT] : T(0);
+              const T s = sq<NT>(st_at(0), ((r * 8 + j) * NST0));
+              const T c = C::SIN ? sq<NT>(st_at(0), ((r * 8 + j) * NST0 + 1)) : T(0);
               T d1, d2;
               act_d12<ACT>(s, c, d1, d2);
               zb[r][j] = sb[r][j] * d1;
