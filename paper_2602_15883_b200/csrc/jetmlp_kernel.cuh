@@ -134,11 +134,13 @@ struct JetCfg {
   static constexpr int PP = JET ? 1 : RPT;      // points per thread
   static constexpr int SIN = (ACT == ACT_SIN) ? 1 : 0;
   static constexpr int NST0 = 1 + SIN;                       // layer-0 stash / (point,unit)
-  // hidden-layer stash per (point, unit), jet modes: the layer's S output
-  // streams (rebuild the next layer's input without recomputation) and S
-  // adjoint factors {d1, d2*z_g[i], d3*z_g[j]^2 + d2*z_l[j]} so the activation
-  // adjoint is a handful of FMAs
-  static constexpr int NSTH = JET ? 2 * S : NST0;
+  // hidden-layer stash per (point, unit), jet modes: sigma(z_v) [cos z_v for
+  // sin] and the pre-activation derivative streams z_g[NG], z_l[NL] -- enough
+  // to rebuild both the layer's S output streams (the next layer's dW input)
+  // and its adjoint factors {d1, d2 z_g, d3 z_g^2 + d2 z_l} with the forward's
+  // own expressions, at half the footprint of storing both (the stash then
+  // stays L2-resident)
+  static constexpr int NSTH = JET ? S + SIN : NST0;
   // k-quad layout: element (row, k) at (k>>2)*RS4 + row*4 + (k&3).  RS4 is
   // padded so that consecutive quads start 4 banks apart: the 8 lanes of a
   // quarter-warp touching 8 consecutive quads then cover all 32 banks.
@@ -617,20 +619,13 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             outv[1 + NG + i][j] = d2 * zg * zg + d1 * acc[1 + NG + i][j];
           }
           if constexpr (BWD) {
-            // one run of 2S: the S output streams, then the S adjoint factors
-            static_assert(NSTH == 2 * S && 1 + NG + NL == S, "jet stash run layout");
-            const T d3 = act_d3<ACT>(s, c, d1, d2);
-            T sv[2 * S];
+            // one run: s, [c], z_g[0..NG), z_l[0..NL)
+            static_assert(NSTH == S + C::SIN && 1 + NG + NL == S, "jet stash run layout");
+            T sv[NSTH];
+            sv[0] = s;
+            if constexpr (C::SIN) sv[1] = c;
 #pragma unroll
-            for (int st = 0; st < S; ++st) sv[st] = outv[st][j];
-            sv[S] = d1;
-#pragma unroll
-            for (int i = 0; i < NG; ++i) sv[S + 1 + i] = d2 * acc[1 + i][j];
-#pragma unroll
-            for (int i = 0; i < NL; ++i) {
-              const T zg = acc[1 + LAP0 + i][j];
-              sv[S + 1 + NG + i] = d3 * zg * zg + d2 * acc[1 + NG + i][j];
-            }
+            for (int i = 0; i < NG + NL; ++i) sv[1 + C::SIN + i] = acc[1 + i][j];
             st_run<NT>(st_at(l), j * NSTH, sv);
           }
         } else {
@@ -850,15 +845,22 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if constexpr (JET) {
-              // numpy_backend.py:58-89 with the forward-time factors
-              T fv[S];
-              ld_run<NT>(fv, st_at(l), j * NSTH + S);
-              const T d1 = fv[0];
+              // numpy_backend.py:58-89, factors rebuilt from the stashed jet
+              T fv[NSTH];
+              ld_run<NT>(fv, st_at(l), j * NSTH);
+              const T sj = fv[0], cj = C::SIN ? fv[1] : T(0);
+              T d1, d2;
+              act_d12<ACT>(sj, cj, d1, d2);
+              const T d3 = act_d3<ACT>(sj, cj, d1, d2);
+              const T* zgv = fv + 1 + C::SIN;
               T ga[NG], lb[NL > 0 ? NL : 1];
 #pragma unroll
-              for (int i = 0; i < NG; ++i) ga[i] = fv[1 + i];
+              for (int i = 0; i < NG; ++i) ga[i] = d2 * zgv[i];
 #pragma unroll
-              for (int i = 0; i < NL; ++i) lb[i] = fv[1 + NG + i];
+              for (int i = 0; i < NL; ++i) {
+                const T zg = zgv[LAP0 + i];
+                lb[i] = d3 * zg * zg + d2 * zgv[NG + i];
+              }
               T zv = sb[0][j] * d1;
 #pragma unroll
               for (int i = 0; i < NG; ++i) zv += sb[1 + i][j] * ga[i];
@@ -912,12 +914,20 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                   hv[1 + NG + i][j] = d2 * zg * zg;
                 }
               } else {
+                // the layer's output streams, rebuilt as in the forward epilogue
+                T hvv[NSTH];
+                ld_run<NT>(hvv, st_at(lp), j * NSTH);
+                const T sj = hvv[0], cj = C::SIN ? hvv[1] : T(0);
+                T d1, d2;
+                act_d12<ACT>(sj, cj, d1, d2);
+                const T* zgv = hvv + 1 + C::SIN;
+                hv[0][j] = sj;
 #pragma unroll
-                {
-                  T hvv[S];
-                  ld_run<NT>(hvv, st_at(lp), j * NSTH);
+                for (int i = 0; i < NG; ++i) hv[1 + i][j] = d1 * zgv[i];
 #pragma unroll
-                  for (int st = 0; st < S; ++st) hv[st][j] = hvv[st];
+                for (int i = 0; i < NL; ++i) {
+                  const T zg = zgv[LAP0 + i];
+                  hv[1 + NG + i][j] = d2 * zg * zg + d1 * zgv[NG + i];
                 }
               }
             } else {

@@ -175,14 +175,18 @@ class LocalTrainer:
             self.workers[r].enqueue_epoch(gate=self.gate_args[r] if self.workers[r].objective.ghost else None)
         cur.wait_stream(self.comm)
 
-    def _graph(self, exchange):
-        g = self.graphs.get(exchange)
+    def _graph(self, exchange, epochs=1):
+        """CUDA graph of `epochs` consecutive epochs, the first with the
+        exchange iff `exchange` (a whole comm_interval block is one replay)."""
+        key = (exchange, epochs)
+        g = self.graphs.get(key)
         if g is None:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._enqueue(exchange)
-            self.graphs[exchange] = g
+                for i in range(epochs):
+                    self._enqueue(exchange and i == 0)
+            self.graphs[key] = g
         return g
 
     def check_flags(self):
@@ -193,12 +197,22 @@ class LocalTrainer:
         for w in self.workers.values():
             w.exchange_log.append((e, sorted(w.expected_messages)))
 
-    def run(self, epochs, start=0, use_graphs=True, record_times=True):
-        """Train `epochs` epochs; returns per-epoch device times (s)."""
+    def run(self, epochs, start=0, use_graphs=True, record_times=True, unroll=False):
+        """Train `epochs` epochs; returns per-epoch device times (s).
+
+        unroll=True (needs record_times=False) replays each whole
+        comm_interval block -- the exchange epoch and the comm_interval - 1
+        epochs that reuse its targets -- as ONE graph."""
         comm = self.plan.train_config.comm_interval
+        if unroll and record_times:
+            raise ValueError("unrolled graph blocks are timed as a whole; use record_times=False")
         events = []
-        for i, e in enumerate(range(start, start + epochs)):
+        e, end = start, start + epochs
+        while e < end:
             exchange = e % comm == 0
+            block = 1
+            if unroll and use_graphs and self._ran_eager and exchange and e + comm <= end:
+                block = comm
             if record_times:
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record()
@@ -207,14 +221,15 @@ class LocalTrainer:
             # lazily set attribute); later epochs replay captured graphs of the
             # same work
             if use_graphs and self._ran_eager:
-                self._graph(exchange).replay()
+                self._graph(exchange, block).replay()
             else:
                 self._enqueue(exchange)
                 self._ran_eager = True
             if exchange:
                 self.log_exchange(e)
             for w in self.workers.values():
-                w.epochs_done += 1
+                w.epochs_done += block
+            e += block
         if not record_times:
             return None  # asynchronous: caller synchronises and calls check_flags()
         ev = torch.cuda.Event(enable_timing=True)

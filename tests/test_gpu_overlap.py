@@ -65,3 +65,30 @@ def test_gate_timeout_flags_deadlock(golden):
     assert int(w.flags.item()) & X.FLAG_EXCHANGE_TIMEOUT
     with pytest.raises(DeadlockError):
         w.check_flags()
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_unrolled_comm_interval_blocks_bit_identical(overlap):
+    """comm_interval = 3: replaying each exchange block (1 exchange epoch +
+    2 epochs on the same targets) as one CUDA graph changes nothing."""
+    from paper_2602_15883_b200 import config as fconfig
+    from paper_2602_15883_b200.runtime import TrainConfig, build_plan
+    from paper_2602_15883_b200.runtime.driver import LocalTrainer
+
+    pb = fconfig.cylinder2d_problem(n_pde=2000, n_ghost=40, per_snapshot=12, grid_nx=9, snapshots=10,
+                                    hidden_layers=2, width=32, activation="tanh", counts=(2, 1), time_splits=2)
+    tc = TrainConfig(epochs=8, batch_size=500, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor,
+                     lr_factor=0.5, lr_interval=3, comm_interval=3, seed=0)
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
+    a = LocalTrainer(plan, overlap=overlap)
+    a.run(8)
+    b = LocalTrainer(plan, overlap=overlap)
+    b.run(8, use_graphs=True, record_times=False, unroll=True)
+    assert (True, 3) in b.graphs
+    for r in a.workers:
+        wa, wb = a.workers[r], b.workers[r]
+        assert np.array_equal(wa.flat.cpu().numpy(), wb.flat.cpu().numpy()), r
+        wa.sync_history()
+        wb.sync_history()
+        assert np.array_equal(np.array(wa.history)[:, 1:], np.array(wb.history)[:, 1:]), r
+        assert wa.exchange_log == wb.exchange_log
