@@ -345,7 +345,7 @@ def run_ours(args):
                 "flops_per_point": fpp, "points_per_launch": n_loc, "value_points_per_launch": pde["n_mse"],
                 "flops_per_launch": flops_launch,
                 "kernel_ms": pde["ms"], "kernel_share_of_step": pde["ms"] / (t_rank / args.steps * 1e3),
-                "traffic": None,
+                "traffic": _traffic(args.config, n_sub, world),
             },
             **({"hbm": hbm} if hbm else {}),
             "clocks": clk,
@@ -356,6 +356,20 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _traffic(config_id, n_sub, world):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum
+    of the same bench command), or None when that config was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    key = f"{config_id}/P{n_sub}" + ("" if world == 1 else f"/N{world}")
+    e = t.get(key)
+    return None if e is None else e["dram_read_bytes"] + e["dram_write_bytes"]
 
 
 def _launches_per_epoch(trainer, X):

@@ -263,35 +263,57 @@ __device__ __forceinline__ void f2_lds(f32x2& p0, f32x2& p1, const float* src) {
   p1 = v.y;
 }
 
+// FP32 core of gemm_rows: unit pairs (0,1) (2,3) (4,5) (6,7) accumulate as
+// FFMA2 with the row activation broadcast; the per-element fma chain (k
+// ascending) is the same as the scalar path's.  acc2[r][q] = units
+// unit_of(g, 2q), unit_of(g, 2q + 1) of row rg*RPT + r.
+template <int W, int RPT, int RS4>
+__device__ __forceinline__ void gemm_rows_f2(const float* __restrict__ A, const float* __restrict__ B, int rg, int g,
+                                             f32x2 (&acc2)[RPT][4]) {
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc2[r][q] = 0ull;
+  const float* ap = A + rg * (4 * RPT);
+  const float* bp = B + 4 * g;
+#pragma unroll kGemmUnroll
+  for (int kq = 0; kq < W / 4; ++kq) {
+    float av[4 * RPT];
+    vload(av, ap + kq * RS4);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      f32x2 b[4];
+      f2_lds(b[0], b[1], bp + (4 * kq + kk) * W);
+      f2_lds(b[2], b[3], bp + (4 * kq + kk) * W + W / 2);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f2_fma(acc2[r][q], av[4 * r + kk], b[q]);
+    }
+  }
+}
+
+// store_block for packed pairs: row r's units {4g..4g+3} are (acc2[r][0], acc2[r][1])
+// and {W/2+4g..} are (acc2[r][2], acc2[r][3]) -- 16 contiguous bytes each, so
+// the pairs go to shared memory as they are (no unpacking moves)
+template <int W, int RPT, int RS4>
+__device__ __forceinline__ void store_block_f2(float* __restrict__ buf, int rg, int g, const f32x2 (&acc2)[RPT][4]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* dst = buf + (g + h * (W / 8)) * RS4 + rg * (4 * RPT);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      *reinterpret_cast<ulonglong2*>(dst + 4 * r) = make_ulonglong2(acc2[r][2 * h], acc2[r][2 * h + 1]);
+  }
+}
+
 // acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][unit_of(g, j)]
 template <typename T, int W, int RPT, int RS4>
 __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
                                           T (&acc)[RPT][8]) {
   if constexpr (sizeof(T) == 4) {
-    // FP32: unit pairs (0,1) (2,3) (4,5) (6,7) accumulate as FFMA2 with the row
-    // activation broadcast; same per-element fma chain (k ascending) as below
     f32x2 acc2[RPT][4];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc2[r][q] = 0ull;
-    const float* ap = reinterpret_cast<const float*>(A) + rg * (4 * RPT);
-    const float* bp = reinterpret_cast<const float*>(B) + 4 * g;
-#pragma unroll kGemmUnroll
-    for (int kq = 0; kq < W / 4; ++kq) {
-      float av[4 * RPT];
-      vload(av, ap + kq * RS4);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        f32x2 b[4];
-        f2_lds(b[0], b[1], bp + (4 * kq + kk) * W);
-        f2_lds(b[2], b[3], bp + (4 * kq + kk) * W + W / 2);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) f2_fma(acc2[r][q], av[4 * r + kk], b[q]);
-      }
-    }
+    gemm_rows_f2<W, RPT, RS4>(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B), rg, g, acc2);
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -1052,11 +1074,20 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         // dX: S-bar_{l-1} = Zbar_l W_l^T
         {
           const T* Bm = (ws & 1) ? slot1 : slot0;
-          T acc[RPT][8];
-          gemm_rows<T, W, RPT, RS4>(Gs, Bm, rg, g, acc);
-          __syncthreads();
-          FR_MARK(10);
-          store_block<T, W, RPT, RS4>(Gs, rg, g, acc);
+          if constexpr (sizeof(T) == 4) {
+            f32x2 acc2[RPT][4];
+            gemm_rows_f2<W, RPT, RS4>(reinterpret_cast<const float*>(Gs), reinterpret_cast<const float*>(Bm), rg,
+                                      g, acc2);
+            __syncthreads();
+            FR_MARK(10);
+            store_block_f2<W, RPT, RS4>(reinterpret_cast<float*>(Gs), rg, g, acc2);
+          } else {
+            T acc[RPT][8];
+            gemm_rows<T, W, RPT, RS4>(Gs, Bm, rg, g, acc);
+            __syncthreads();
+            FR_MARK(10);
+            store_block<T, W, RPT, RS4>(Gs, rg, g, acc);
+          }
         }
         cp_async_wait_all();
         __syncthreads();
