@@ -221,6 +221,7 @@ def run_ours(args):
     e += args.warmup
     barrier()
     X.launch_count = 0
+    k0 = X.kernel_launches()
     times = []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
@@ -234,6 +235,7 @@ def run_ours(args):
         barrier()
     t_rank = sum(a.elapsed_time(b) for a, b in times) * 1e-3
     launches_host = X.launch_count
+    launches_timed = X.kernel_launches() - k0  # eager launches (graph replays are counted at capture)
     t_max = t_rank
     if dist is not None:
         tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
@@ -245,7 +247,7 @@ def run_ours(args):
     if world == 1:
         lp = _launches_per_epoch(trainer, X)
     else:
-        lp = None
+        lp = launches_timed / args.steps  # no graphs: the library counted every launch
 
     # ---- e2e: host pinned inputs copied in + loss row copied out every step ----
     obj = worker.objective
@@ -329,7 +331,7 @@ def run_ours(args):
             },
             "e2e": {"value": args.n_pde * args.e2e_steps / t_e2e, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 56},
-            "gpu_launches": (lp * args.steps) if lp is not None else None,
+            "gpu_launches": int(round(lp * args.steps)) if lp is not None else None,
             "launches_per_step": lp,
             "roofline": {
                 "bound": "tensor" if tf32 else "compute",
