@@ -653,37 +653,6 @@ struct SegRows {
   int n;
   int rows[8];
 };
-__global__ void reduce_loss_kernel(const double* __restrict__ lpart, SegRows seg, double* sums) {
-  const int s = threadIdx.x;
-  if (s >= seg.n) return;
-  int r0 = 0;
-  for (int i = 0; i < s; ++i) r0 += seg.rows[i];
-  double a = 0.0, b = 0.0;
-  for (int r = r0; r < r0 + seg.rows[s]; ++r) {
-    a += lpart[2 * r];
-    b += lpart[2 * r + 1];
-  }
-  sums[2 * s] = a;
-  sums[2 * s + 1] = b;
-}
-
-extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int n_seg, double* sums,
-                              fr_stream_t stream) {
-  if (!sums || !seg_rows_host || n_seg < 1 || n_seg > 8) return fail("fr_reduce_loss: bad arguments");
-  SegRows seg{};
-  seg.n = n_seg;
-  int total = 0;
-  for (int i = 0; i < n_seg; ++i) {
-    seg.rows[i] = seg_rows_host[i];
-    total += seg_rows_host[i];
-  }
-  if (total > 0 && !lpart) return fail("fr_reduce_loss: NULL lpart");
-  reduce_loss_kernel<<<1, 32, 0, stream>>>(lpart, seg, sums);
-  ++g_kernel_launches;
-  FR_CUDA(cudaGetLastError(), "fr_reduce_loss");
-  return 0;
-}
-
 // ---------------------------------------------------------------------------
 // Adam (optim.py:20-49) with the epoch bookkeeping of objective.py:183-198 and
 // worker.py:231-244.  Multi-CTA: every block redundantly forms the global norm
@@ -705,6 +674,46 @@ __device__ double block_sum_fixed(double v, double* red) {
   const double r = red[0];
   __syncthreads();
   return r;
+}
+
+// One block per segment, the same strided partial sums + fixed tree as the
+// optimiser kernel's loss reduction below, so `sums` equals the history row's
+// parts bit for bit (and the wide path's tens of thousands of tile rows reduce
+// in parallel).
+__global__ void __launch_bounds__(ADAM_NT) reduce_loss_kernel(const double* __restrict__ lpart, SegRows seg,
+                                                              double* sums) {
+  __shared__ double red[ADAM_NT];
+  const int s = blockIdx.x;
+  int r0 = 0;
+  for (int i = 0; i < s; ++i) r0 += seg.rows[i];
+  double x = 0.0, y = 0.0;
+  for (int r = r0 + threadIdx.x; r < r0 + seg.rows[s]; r += ADAM_NT) {
+    x += lpart[2 * r];
+    y += lpart[2 * r + 1];
+  }
+  x = block_sum_fixed(x, red);
+  y = block_sum_fixed(y, red);
+  if (threadIdx.x == 0) {
+    sums[2 * s] = x;
+    sums[2 * s + 1] = y;
+  }
+}
+
+extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int n_seg, double* sums,
+                              fr_stream_t stream) {
+  if (!sums || !seg_rows_host || n_seg < 1 || n_seg > 8) return fail("fr_reduce_loss: bad arguments");
+  SegRows seg{};
+  seg.n = n_seg;
+  int total = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    seg.rows[i] = seg_rows_host[i];
+    total += seg_rows_host[i];
+  }
+  if (total > 0 && !lpart) return fail("fr_reduce_loss: NULL lpart");
+  reduce_loss_kernel<<<n_seg, ADAM_NT, 0, stream>>>(lpart, seg, sums);
+  ++g_kernel_launches;
+  FR_CUDA(cudaGetLastError(), "fr_reduce_loss");
+  return 0;
 }
 
 template <typename T>
