@@ -26,6 +26,11 @@ import time
 
 import numpy as np
 
+# separate hardware queues for the compute, transport and NCCL streams: a
+# gated epoch kernel spins until the transport stream signals, which must never
+# sit in the same hardware queue behind it (read at CUDA context creation)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -493,6 +493,19 @@ extern "C" int fr_epoch_workspace_capped(const fr_plan* p, long long n_colloc, c
   return 0;
 }
 
+__global__ void signal_kernel(unsigned* word, unsigned value, unsigned delay_ns) {
+  if (delay_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      __nanosleep(1000);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < delay_ns);
+  }
+  __threadfence_system();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(word), "r"(value) : "memory");
+}
+
 extern "C" int fr_epoch_fwd_bwd(const fr_plan* p, const void* kparams, const void* colloc, long long n_colloc,
                                 double pde_coef, const fr_mse_set* sets, int n_set_count, const double* vel_w,
                                 double* gpart, double* const* lpart_blocks, void* scratch, fr_stream_t stream) {
@@ -510,6 +523,13 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
   if (gate && (!gate->gate || gate->first_gated_set < 0 || gate->max_ctas < 0))
     return fail("fr_epoch_fwd_bwd_gated: bad gate");
   if (gate && p->info.width_pad > 64) return fail("fr_epoch_fwd_bwd_gated: fused epoch path only (width <= 64)");
+  if (gate) {
+    // the transport's signal kernel must be resident before a kernel that spins
+    // on it is running: with lazy module loading (CUDA_MODULE_LOADING=LAZY, the
+    // default) its first launch would otherwise wait for the device to idle
+    cudaFuncAttributes fa;
+    FR_CUDA(cudaFuncGetAttributes(&fa, signal_kernel), "fr_epoch_fwd_bwd_gated: preload fr_signal");
+  }
   long long ns[3] = {0, 0, 0};
   for (int i = 0; i < n_set_count; ++i) {
     if (sets[i].n < 0 || (sets[i].n > 0 && (!sets[i].pts || !sets[i].target_u)))
@@ -558,19 +578,6 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
     }
   }
   return epoch_call(p, &e, ws.grid, stream, nullptr);
-}
-
-__global__ void signal_kernel(unsigned* word, unsigned value, unsigned delay_ns) {
-  if (delay_ns) {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    do {
-      __nanosleep(1000);
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    } while (t - t0 < delay_ns);
-  }
-  __threadfence_system();
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(word), "r"(value) : "memory");
 }
 
 extern "C" int fr_signal(unsigned* word, unsigned value, unsigned delay_ns, fr_stream_t stream) {

@@ -282,16 +282,18 @@ def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
 class DistributedTrainer:
     """This process's rank of a torch.distributed group (NCCL over NVLink).
 
-    overlap=True (default for the fused small-width kernel): the ghost
-    exchange is overlapped with the interior work.  The producer and pack run
-    on the compute stream; the NCCL send/recv group then runs on a transport
-    stream which, once the receives have landed, sets this rank's gate word
-    (fr_signal).  The epoch kernel is launched immediately with its persistent
-    grid capped `reserve_sms` below the SM count (so NCCL's kernels have SMs to
-    run on); every CTA walks its PDE and observation tiles first and only its
-    ghost tiles wait on the gate, so the transfer hides under the interior
-    residual work.  The first exchange runs in stream order (it also brings up
-    the NCCL connections, which may synchronise the device)."""
+    overlap=True (default for the fused small-width kernel): the whole ghost
+    round is overlapped with the interior work.  The producer (value forward
+    of the neighbours' ghost points), the pack and the NCCL send/recv group all
+    run on a transport stream which, once the receives have landed, sets this
+    rank's gate word (fr_signal).  The epoch kernel is launched at once on the
+    compute stream with its persistent grid capped `reserve_sms` below the SM
+    count (so the producer's and NCCL's kernels have SMs to run on); every CTA
+    walks its PDE and observation tiles first and only its ghost tiles wait on
+    the gate, so producer + transfer hide under the interior residual work.
+    The optimiser waits for the transport stream (the producer read the
+    pre-update parameters).  The first exchange runs in stream order (it also
+    brings up the NCCL connections, which may synchronise the device)."""
 
     def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=2):
         import torch.distributed as dist
@@ -320,29 +322,39 @@ class DistributedTrainer:
         """Exchange (if due) then the fused epoch (overlapped, see the class doc)."""
         w = self.worker
         exchange = e % self.plan.train_config.comm_interval == 0
-        gate = None
-        if exchange:
-            w.produce()
-            for k, _ in enumerate(self.sends):
-                w.pack_edge(k, *self.send_bufs[k])
-            if self.overlap and self._connected:
-                cur = torch.cuda.current_stream()
-                self.gate_word.zero_()
-                self.comm.wait_stream(cur)
+        cur = torch.cuda.current_stream()
+        if exchange and self.overlap and self._connected:
+            # the epoch kernel is enqueued first so that it takes its capped
+            # grid; the producer and NCCL then run on the reserved SMs
+            self.gate_word.zero_()
+            ready = torch.cuda.Event()
+            ready.record(cur)  # parameters after the previous update; gate reset
+            w.objective.mark_targets_set()
+
+            def transport():
+                self.comm.wait_event(ready)
                 with torch.cuda.stream(self.comm):
+                    w.produce(stream=self.comm)
+                    for k, _ in enumerate(self.sends):
+                        w.pack_edge(k, *self.send_bufs[k], stream=self.comm)
                     for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                         wk.wait()  # transport stream waits for the transfers
                     X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
-                gate = self.gate
-            else:
+                # the optimiser rewrites the parameters the producer read, and the
+                # next round reuses the send buffers and targets
+                cur.wait_stream(self.comm)
+
+            w.enqueue_epoch(gate=self.gate, before_update=transport)
+        else:
+            if exchange:
+                w.produce()
+                for k, _ in enumerate(self.sends):
+                    w.pack_edge(k, *self.send_bufs[k])
                 for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                     wk.wait()  # orders the compute stream after the transfers (no host sync)
                 self._connected = True
-            w.objective.mark_targets_set()
-        w.enqueue_epoch(gate=gate)
-        if gate is not None:
-            # send buffers / targets are reused by the next round
-            torch.cuda.current_stream().wait_stream(self.comm)
+                w.objective.mark_targets_set()
+            w.enqueue_epoch()
         w.epochs_done += 1
         if exchange:
             w.exchange_log.append((e, sorted(w.expected_messages)))

@@ -1,6 +1,13 @@
 import os
 import sys
 
+# The emulated multi-rank tests run up to 8 ranks as threads of one process,
+# each with a compute and a transport stream; with the default 8 hardware work
+# queues, unrelated streams would share a queue and a spinning gated kernel
+# could block another rank's transport behind it.  (One process per GPU, as in
+# production, uses three streams.)  Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 
