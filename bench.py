@@ -225,22 +225,35 @@ def run_ours(args):
     run_epochs(e, args.warmup)  # first epoch eager + graph capture happen here
     e += args.warmup
     barrier()
+    # a device-side pause (1 ms, outside the events) after each flush lets the
+    # host finish enqueuing the step before the GPU reaches it, as in steady
+    # training where the host runs ahead; the host enqueue time per step is
+    # reported beside it, so a host-bound step would be visible
+    pause_word = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def pause():
+        X.call("fr_signal", X.ptr(pause_word), 0, 1_000_000, X.stream_ptr())
+
     X.launch_count = 0
     k0 = X.kernel_launches()
     times = []
+    host_s = 0.0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.fill_(1.0)
+            pause()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
+            h0 = time.perf_counter()
             run_epochs(e, 1)
+            host_s += time.perf_counter() - h0
             b.record()
             e += 1
             times.append((a, b))
         barrier()
     t_rank = sum(a.elapsed_time(b) for a, b in times) * 1e-3
-    launches_host = X.launch_count
-    launches_timed = X.kernel_launches() - k0  # eager launches (graph replays are counted at capture)
+    launches_host = X.launch_count - args.steps  # minus the pauses
+    launches_timed = X.kernel_launches() - k0 - args.steps  # eager launches (graph replays are counted at capture)
     t_max = t_rank
     if dist is not None:
         tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
@@ -357,6 +370,7 @@ def run_ours(args):
             **({"hbm": hbm} if hbm else {}),
             "clocks": clk,
             "host_launches_timed": launches_host,
+            "host_enqueue_ms_per_step": host_s / args.steps * 1e3,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_seconds)
