@@ -476,13 +476,11 @@ def _reference_module():
     return "port"
 
 
-def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
-    """Time the reference's LocalObjective.epoch + adam_step on a sample of the
-    P=1 workload (all obs, n_sample collocation points), all host cores."""
-    from threadpoolctl import threadpool_limits
-
+def _reference_epoch(args, n_sample=25_000):
+    """Build (once) the reference's LocalObjective + Adam on a sample of the P=1
+    workload (all obs, n_sample collocation points); returns (step, n_sample,
+    n_obs, kind) where step() runs one epoch (objective + adam_step)."""
     kind = _reference_module()
-    cores = os.cpu_count()
     from paper_2602_15883_b200.config import cylinder2d_problem, cylinder3d_problem
 
     cfgd = CONFIGS[getattr(args, "config", "C")]
@@ -495,61 +493,84 @@ def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
     sample = ds.colloc_points[:n_sample]
     rg = pb.domain.regime
     w = pb.weights
-    t_epochs = []
-    with threadpool_limits(limits=cores):
-        if kind == "reference":
-            from flowrec.decomposition import RankDatasets
-            from flowrec.network import ExpertConfig, init_params
-            from flowrec.physics import FlowRegime, LossWeights
-            from flowrec.runtime import AdamState, LocalObjective, adam_step
+    if kind == "reference":
+        from flowrec.decomposition import RankDatasets
+        from flowrec.network import ExpertConfig, init_params
+        from flowrec.physics import FlowRegime, LossWeights
+        from flowrec.runtime import AdamState, LocalObjective, adam_step
 
-            regime = FlowRegime(rg.kind, rg.reynolds)
-            cfg = ExpertConfig.for_regime(regime, arch["hidden_layers"], arch["width"], arch["activation"])
-            lw = LossWeights(w.obs, w.pde, w.ghost_u, w.ghost_p_space, w.ghost_p_time, velocity=w.velocity)
-            obj = LocalObjective(cfg, regime, RankDatasets(ds.obs_points, ds.obs_velocity, sample, ()), lw, 25000)
-            params = init_params(cfg, 0)
-            st = AdamState.zeros(cfg.n_params)
-            rng = np.random.default_rng(0)
-            t_end = time.perf_counter() + budget_s
-            while time.perf_counter() < t_end or not t_epochs:
-                t0 = time.perf_counter()
-                _, g, _ = obj.epoch(params, rng)
-                adam_step(params.flat, g, st, 1e-3)
-                t_epochs.append(time.perf_counter() - t0)
-        else:
-            from oracle import flowrec_oracle as O
-            from paper_2602_15883_b200.network import init_params
+        regime = FlowRegime(rg.kind, rg.reynolds)
+        cfg = ExpertConfig.for_regime(regime, arch["hidden_layers"], arch["width"], arch["activation"])
+        lw = LossWeights(w.obs, w.pde, w.ghost_u, w.ghost_p_space, w.ghost_p_time, velocity=w.velocity)
+        obj = LocalObjective(cfg, regime, RankDatasets(ds.obs_points, ds.obs_velocity, sample, ()), lw, 25000)
+        params = init_params(cfg, 0)
+        st = AdamState.zeros(cfg.n_params)
+        rng = np.random.default_rng(0)
 
-            flat = init_params(pb.expert_config, 0).flat.copy()
-            m, v = np.zeros_like(flat), np.zeros_like(flat)
-            data = dict(obs_pts=ds.obs_points, obs_vel=ds.obs_velocity, colloc=sample, ghosts=[])
-            wd = dict(obs=w.obs, pde=w.pde, ghost_u=w.ghost_u, ghost_p_space=w.ghost_p_space,
-                      ghost_p_time=w.ghost_p_time, velocity=w.velocity)
-            t_end = time.perf_counter() + budget_s
-            step = 0
-            while time.perf_counter() < t_end or not t_epochs:
-                t0 = time.perf_counter()
-                _, g, _ = O.local_epoch(flat, pb.expert_config.arch, arch["activation"], rg.kind, rg.reynolds,
-                                        data, wd)
-                step, _ = O.adam_update(flat, g, m, v, step, 1e-3)
-                t_epochs.append(time.perf_counter() - t0)
+        def step():
+            _, g, _ = obj.epoch(params, rng)
+            adam_step(params.flat, g, st, 1e-3)
+    else:
+        from oracle import flowrec_oracle as O
+        from paper_2602_15883_b200.network import init_params
+
+        flat = init_params(pb.expert_config, 0).flat.copy()
+        m, v = np.zeros_like(flat), np.zeros_like(flat)
+        data = dict(obs_pts=ds.obs_points, obs_vel=ds.obs_velocity, colloc=sample, ghosts=[])
+        wd = dict(obs=w.obs, pde=w.pde, ghost_u=w.ghost_u, ghost_p_space=w.ghost_p_space,
+                  ghost_p_time=w.ghost_p_time, velocity=w.velocity)
+        state = {"step": 0}
+
+        def step():
+            _, g, _ = O.local_epoch(flat, pb.expert_config.arch, arch["activation"], rg.kind, rg.reynolds, data, wd)
+            state["step"], _ = O.adam_update(flat, g, m, v, state["step"], 1e-3)
+
+    return step, n_sample, ds.n_obs, kind
+
+
+def _baseline_record(args, t_epochs, n_sample, n_obs, kind):
+    cores = os.cpu_count()
     t = float(np.median(t_epochs))
     return {"value": n_sample / t, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"P=1 epoch (LocalObjective.epoch + adam_step) on {n_sample} of {args.n_pde} "
-                      f"collocation points + all {ds.n_obs} observations, {len(t_epochs)} epochs, "
+                      f"collocation points + all {n_obs} observations, {len(t_epochs)} epochs, "
                       f"median {t:.3f} s/epoch, BLAS threads={cores}",
             "s_per_epoch_sample": t}
 
 
+def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
+    """Time the reference's LocalObjective.epoch + adam_step on a sample of the
+    P=1 workload (all obs, n_sample collocation points), all host cores, for
+    about budget_s seconds."""
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=os.cpu_count()):
+        step, n_sample, n_obs, kind = _reference_epoch(args, n_sample)
+        t_epochs = []
+        t_end = time.perf_counter() + budget_s
+        while time.perf_counter() < t_end or not t_epochs:
+            t0 = time.perf_counter()
+            step()
+            t_epochs.append(time.perf_counter() - t0)
+    return _baseline_record(args, t_epochs, n_sample, n_obs, kind)
+
+
 def run_reference(args):
+    from threadpoolctl import threadpool_limits
+
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    vals = []
-    for _ in range(args.warmup):
-        cpu_baseline(args, budget_s=0.0)
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(args, budget_s=0.0))
+    with threadpool_limits(limits=os.cpu_count()):
+        step, n_sample, n_obs, kind = _reference_epoch(args)
+        for _ in range(args.warmup):
+            step()
+        t_epochs = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            step()
+            t_epochs.append(time.perf_counter() - t0)
+    vals = [_baseline_record(args, t_epochs, n_sample, n_obs, kind)]
     v = float(np.median([x["value"] for x in vals]))
     cb = dict(vals[-1])
     cb["value"] = v
