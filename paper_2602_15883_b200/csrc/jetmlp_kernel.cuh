@@ -620,7 +620,10 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       stage(ws + 1);
       T acc[RPT][8];
       gemm_rows<T, W, RPT, RS4>(Xs, Bm, rg, g, acc);
-      __syncthreads();
+      // training modes ping-pong the layer input / output between Xs and Gs
+      // (Gs is idle in the forward sweep), so a warp's epilogue never waits
+      // for the slower warps' GEMM; single-buffer modes sync here
+      if constexpr (!BWD) __syncthreads();
       FR_MARK(2);
       T outv[RPT][8];
 #pragma unroll
@@ -664,10 +667,15 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           }
         }
       }
-      store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
+      store_block<T, W, RPT, RS4>(BWD ? Gs : Xs, rg, g, outv);
       cp_async_wait_all();
       __syncthreads();
       FR_MARK(3);
+      if constexpr (BWD) {
+        T* t = Xs;  // this layer's output becomes the next layer's input
+        Xs = Gs;
+        Gs = t;
+      }
       ++ws;
     }
 
