@@ -274,20 +274,40 @@ def run_ours(args):
     host_bufs = [b.cpu().pin_memory() for b in dev_bufs]
     h2d = sum(b.numel() * b.element_size() for b in host_bufs)
     row_host = torch.empty(7, dtype=torch.float64).pin_memory()
+    # inputs stream in the way a training data loader feeds the step: step k+1's
+    # host->device copy runs on a copy stream into a staging set while step k
+    # computes; each step starts with a device-side move (staging -> resident
+    # buffers, ~2 us).  Timed from the first copy to the last result read.
+    staging = [torch.empty_like(d) for d in dev_bufs]
+    copy_stream = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+
+    def prefetch():
+        with torch.cuda.stream(copy_stream):
+            for st, h in zip(staging, host_bufs):
+                st.copy_(h, non_blocking=True)
+        landed = torch.cuda.Event()
+        landed.record(copy_stream)
+        return landed
+
     barrier()
-    ev = []
-    for _ in range(args.e2e_steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for d, h in zip(dev_bufs, host_bufs):
-            d.copy_(h, non_blocking=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    copy_stream.wait_event(a)
+    landed = prefetch()
+    for k in range(args.e2e_steps):
+        cur.wait_event(landed)
+        for d, st in zip(dev_bufs, staging):
+            d.copy_(st, non_blocking=True)
+        if k + 1 < args.e2e_steps:
+            copy_stream.wait_stream(cur)  # staging is free again
+            landed = prefetch()
         run_epochs(e, 1)
         row_host.copy_(worker.history_d[e], non_blocking=True)
-        b.record()
         e += 1
-        ev.append((a, b))
+    b.record()
     barrier()
-    t_e2e = sum(a.elapsed_time(b) for a, b in ev) * 1e-3
+    t_e2e = a.elapsed_time(b) * 1e-3
     if dist is not None:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
