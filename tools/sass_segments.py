@@ -41,10 +41,6 @@ def main(path, min_samples=2000):
               f"fma-lanes/instr {s['fma'] / max(s['ins'], 1):4.2f}  [{top}]")
 
 
-if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 2000)
-
-
 def stalls(path, lo, hi):
     """Stall-reason split of the instructions with lo <= address suffix <= hi (hex)."""
     rows = list(csv.reader(open(path)))
@@ -61,3 +57,8 @@ def stalls(path, lo, hi):
                 tot[c] += float(r[ix[c]] or 0)
     T = sum(tot.values())
     return [(c, v / T) for c, v in tot.most_common(8)]
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 2000)
+
