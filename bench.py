@@ -59,29 +59,63 @@ def flops_per_point(S=6, L=4, W=64, d_in=3, n_out=3):
 
 
 class ClockSampler:
-    """Samples nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+    """Samples SM clocks and clock-event (throttle) reasons during the timed
+    region (B200_PROFILING.md clocks line): NVML every 10 ms, or nvidia-smi
+    every 0.2 s when NVML is unavailable."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [reason names])
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvidia-smi"
 
-    def _run(self):
+    def _run_nvml(self, n):
+        h = n.nvmlDeviceGetHandleByIndex(self.index)
+        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+            bits = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), float(mx), [name for name, attr in self.REASONS
+                                                        if bits & getattr(n, attr)]))
+            self._stop.wait(0.01)
+
+    def _run_smi(self):
+        names = [name for name, _ in self.REASONS]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 7 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         [nm for nm, v in zip(names, f[3:7]) if v == "Active"]))
             except Exception:
                 pass
             self._stop.wait(0.2)
+
+    def _run(self):
+        try:
+            import pynvml as n
+
+            n.nvmlInit()
+            self.source = "nvml"
+            try:
+                self._run_nvml(n)
+            finally:
+                n.nvmlShutdown()
+        except Exception:
+            self.source = "nvidia-smi"
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -95,12 +129,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(x[0] for x in self.samples),
+                "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted({r for x in self.samples for r in x[2]}),
+                "samples": len(self.samples), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
