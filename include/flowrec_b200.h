@@ -121,8 +121,9 @@ int fr_epoch_fwd_bwd(const fr_plan* plan, const void* kparams, const void* collo
  * inside the kernel until *gate != 0, which the transport stream sets with
  * fr_signal() once the NCCL receives (or in-process copies) have landed.  Each
  * CTA reaches its ghost tiles only after all of its PDE and obs tiles, so the
- * exchange latency hides under the interior work.  max_ctas caps the persistent
- * grid so the transport's kernels keep free SMs (0 = every SM); the workspace
+ * exchange latency hides under the interior work.  max_ctas caps the SMs the
+ * persistent grid may occupy (its CTAs = that many SMs x CTAs per SM), so the
+ * transport's kernels keep free SMs (0 = every SM); the workspace
  * must be sized with the same cap (fr_epoch_workspace_capped).  A wait longer
  * than timeout_ms or-s FR_FLAG_EXCHANGE_TIMEOUT into *flags and proceeds (the
  * host raises; drop-in for the reference's DeadlockError, driver.py:161-166). */

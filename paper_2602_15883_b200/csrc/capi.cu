@@ -479,7 +479,8 @@ extern "C" int fr_epoch_workspace_capped(const fr_plan* p, long long n_colloc, c
   KInfo ki{};
   if (epoch_info(p, &ki)) return 1;
   int sms = p->info.num_sms > 0 ? p->info.num_sms : 148;
-  if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
+  if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;  // an SM budget: the grid is sms x CTAs per SM
+  sms *= ki.cps;
   long long tiles = (n_colloc + ki.ppt - 1) / ki.ppt;
   for (int i = 0; i < n_set_count; ++i) tiles += (n_sets[i] + ki.ppt_mse - 1) / ki.ppt_mse;
   out->grid = int(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);

@@ -11,6 +11,7 @@ struct KInfo {
   int stash_elems;   // per-CTA stash elements (of T)
   size_t smem;       // dynamic shared memory bytes
   int ppt_mse;       // epoch kernel: points per MSE tile
+  int cps = 1;       // epoch kernel: resident CTAs per SM (persistent grid = SMs x cps)
 };
 
 template <int V>
@@ -60,8 +61,9 @@ int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
 
 template <typename T, int ACT, int REG, int W>
 int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
-  using CP = JetCfg<T, ACT, MODE_PDE, REG, W>;
-  using CM = JetCfg<T, ACT, MODE_MSE, REG, W, CP::NT>;
+  using E = EpochCfg<T, ACT, REG, W>;
+  using CP = JetCfg<T, ACT, MODE_PDE, REG, W, E::NT>;
+  using CM = JetCfg<T, ACT, MODE_MSE, REG, W, E::NT>;
   const size_t smem = CP::smem_bytes(L) > CM::smem_bytes(L) ? CP::smem_bytes(L) : CM::smem_bytes(L);
   const int sp = CP::stash_per_thread(L) > CM::stash_per_thread(L) ? CP::stash_per_thread(L) : CM::stash_per_thread(L);
   if (info) {
@@ -70,12 +72,16 @@ int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L)
     info->ppt_mse = CM::PPT;
     info->stash_elems = CP::NT * sp;
     info->smem = smem;
+    info->cps = E::CPS;
   }
   if (!e) return 0;
   auto k = jetmlp_epoch_kernel<T, ACT, REG, W>;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return int(err);
+    // all of the unified L1/shared array as shared memory, so E::CPS CTAs fit
+    err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (err != cudaSuccess) return int(err);
     smem_set = smem;
   }

@@ -179,13 +179,14 @@ struct JetCfg {
     e += al(ROWS * NOUT);                  // Ys
     if (BWD) e += al(ROWS * NOUT);         // Ybs
     e += al(PPT * DIN);                    // Ps
-    if (MODE == MODE_MSE) e += al(PPT * NVEL) + al(PPT);  // targets
-    if (BWD) e += al(NT);                  // db partials
+    // (MSE targets are read from global in the head; the db partials alias Ys,
+    // which is dead once the head has run)
     return e;
   }
-  __host__ __device__ static size_t smem_bytes(int L) {
-    return size_t(smem_elems(L)) * sizeof(T) + 2 * NT * sizeof(double);
-  }
+  static_assert(!BWD || ROWS * NOUT >= NT, "db partials alias Ys");
+  // the per-thread loss partials of the final reduction alias Xs (free by then)
+  static_assert(XELEMS * sizeof(T) >= 2 * NT * sizeof(double), "loss-reduction scratch must fit in Xs");
+  __host__ __device__ static size_t smem_bytes(int L) { return size_t(smem_elems(L)) * sizeof(T); }
 };
 
 // Ghost-overlap gate (fr_epoch_gate): spin with back-off until the transport
@@ -228,6 +229,9 @@ __device__ __forceinline__ int unit_of(int g, int j) {
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
 
 // FP32 inner-loop unroll factors (tuned on B200; overridable for sweeps)
+#ifndef FR_EPOCH_2CTA
+#define FR_EPOCH_2CTA 0  // two 192-thread CTAs per SM: measured slower (5.89 vs 5.40 ms), kept as a tuning switch
+#endif
 #ifndef FR_GEMM_UNROLL
 #define FR_GEMM_UNROLL 8
 #endif
@@ -478,15 +482,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   T* Ybs = nullptr;
   if constexpr (BWD) { Ybs = sm; sm += C::al(ROWS * NOUT); }
   T* Ps = sm;                      sm += C::al(PPT * DIN);
-  T* Dbs = nullptr;
-  if constexpr (BWD) { Dbs = sm; sm += C::al(NT); }
-  T* TUs = nullptr;
-  T* TPs = nullptr;
-  if constexpr (MODE == MODE_MSE) {
-    TUs = sm; sm += C::al(PPT * NVEL);
-    TPs = sm; sm += C::al(PPT);
-  }
-  double* red = reinterpret_cast<double*>(sm);
+  T* Dbs = Ys;  // hidden-layer db partials: Ys is dead after the head
+  (void)sm;
 
   const int tid = threadIdx.x;
   const int g = tid % G;
@@ -553,15 +550,6 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       const T* pts = static_cast<const T*>(a.pts) + p0 * DIN;
       const long long rem = n - p0;
       for (int i = tid; i < PPT * DIN; i += NT) Ps[i] = (i / DIN < rem) ? pts[i] : T(0);
-      if constexpr (MODE == MODE_MSE) {
-        // L2-coherent loads: ghost targets may land while this kernel runs (gate)
-        const T* tu = static_cast<const T*>(a.tu) + p0 * NVEL;
-        for (int i = tid; i < PPT * NVEL; i += NT) TUs[i] = (i / NVEL < rem) ? __ldcg(tu + i) : T(0);
-        if (a.has_p) {
-          const T* tpp = static_cast<const T*>(a.tp) + p0;
-          for (int i = tid; i < PPT; i += NT) TPs[i] = (i < rem) ? __ldcg(tpp + i) : T(0);
-        }
-      }
     }
     __syncthreads();
     FR_MARK(0);
@@ -786,14 +774,15 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         double squ = 0.0;
 #pragma unroll
         for (int c = 0; c < NVEL; ++c) {
-          const T d = y[c] - TUs[pt * NVEL + c];
+          // L2-coherent loads: ghost targets may land while this kernel runs (gate)
+          const T d = y[c] - __ldcg(static_cast<const T*>(a.tu) + (p0 + pt) * NVEL + c);
           const T w = T(a.velw[c]);
           squ += double(a.velw[c]) * (double(d) * double(d));
           yb[c] = (two_vc * w) * d;
         }
         lacc0 += squ;
         if (a.has_p) {
-          const T d = y[NVEL] - TPs[pt];
+          const T d = y[NVEL] - __ldcg(static_cast<const T*>(a.tp) + p0 + pt);
           lacc1 += double(d) * double(d);
           yb[NVEL] = two_pc * d;
         }
@@ -1178,6 +1167,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
 
   cp_async_wait_all();
   if constexpr (BWD) {
+    double* red = reinterpret_cast<double*>(Xs);  // the last tile ended with a barrier
     red[tid] = lacc0;
     red[NT + tid] = lacc1;
     __syncthreads();
@@ -1221,14 +1211,25 @@ struct EpochArgs {
   int n_mse;
 };
 
+// The epoch kernel runs EpochCfg::CPS CTAs per SM: FP32 W=64 2D uses two
+// 192-thread CTAs (24-point tiles, 111 KB of shared memory each), so one CTA's
+// barrier waits and latency-bound epilogues are filled by the other's GEMMs.
 template <typename T, int ACT, int REG, int W>
-__global__ void __launch_bounds__(JetCfg<T, ACT, MODE_PDE, REG, W>::NT, 1) jetmlp_epoch_kernel(EpochArgs e) {
+struct EpochCfg {
+  static constexpr bool TWO = sizeof(T) == 4 && W == 64 && Streams<MODE_PDE, REG>::RPT <= 6 && FR_EPOCH_2CTA;
+  static constexpr int NT = TWO ? 192 : JetCfg<T, ACT, MODE_PDE, REG, W>::NT;
+  static constexpr int CPS = TWO ? 2 : 1;
+};
+
+template <typename T, int ACT, int REG, int W>
+__global__ void __launch_bounds__(EpochCfg<T, ACT, REG, W>::NT, EpochCfg<T, ACT, REG, W>::CPS)
+    jetmlp_epoch_kernel(EpochArgs e) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NT = JetCfg<T, ACT, MODE_PDE, REG, W>::NT;
+  constexpr int NT = EpochCfg<T, ACT, REG, W>::NT;
   const long long G = gridDim.x, c = blockIdx.x;
   double* gp = e.pde.gpart + size_t(c) * e.pde.np_pad;
   run_tiles<T, ACT, MODE_PDE, REG, W, NT>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c);
-  long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W>::PPT;
+  long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT;
   for (int d = 0; d < e.n_mse; ++d) {
     const long long t0 = ((c - offset) % G + G) % G;
     run_tiles<T, ACT, MODE_MSE, REG, W, NT>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c);
