@@ -42,7 +42,7 @@ typedef struct fr_plan fr_plan;
 enum { FR_ACT_TANH = 0, FR_ACT_SIN = 1 };                                /* _kernels ACT_* */
 enum { FR_STEADY2D = 0, FR_UNSTEADY2D = 1, FR_UNSTEADY3D = 2 };          /* physics._KINDS */
 enum { FR_F32 = 0, FR_F64 = 1 };
-enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3 };
+enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3, FR_MODE_GJ = 4 };
 enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2, FR_FLAG_EXCHANGE_TIMEOUT = 4 };
 /* contraction math of the training kernels: FP32 SIMT (oracle parity ~1e-5) or
  * TF32 tcgen05 tensor cores (wide FP32 experts, 64 < width <= 512; default) */
@@ -145,6 +145,15 @@ int fr_epoch_fwd_bwd_gated(const fr_plan* plan, const void* kparams, const void*
  * single-thread kernel, release ordering); with delay_ns > 0 it first sleeps
  * that long on the device (tests emulate a slow transport with it) */
 int fr_signal(unsigned* word, unsigned value, unsigned delay_ns, fr_stream_t stream);
+
+/* Ghost-derivative matching (opt-in extension of the reference's value-only
+ * coupling, worker.py:179-197): loss sum_n sum_i sum_c
+ * w_c (d u_c / d x_i (pts_n) - target_du[n][i][c])^2 over the first
+ * derivatives of the velocity w.r.t. every input, times coef in the gradient;
+ * gpart / lpart / scratch as for fr_pde_fwd_bwd (workspace of FR_MODE_GJ). */
+int fr_ghost_jet_fwd_bwd(const fr_plan* plan, const void* kparams, const void* pts, const void* target_du,
+                         long long n, const double* vel_w, double coef, double* gpart, double* lpart, void* scratch,
+                         fr_stream_t stream);
 
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,

@@ -209,6 +209,27 @@ def mse_loss_grad(flat, arch, act, pts, target_u, target_p, vel_w, vel_coef, p_c
     return sq_u, sq_p, jet_backward(flat, arch, act, cache, {"v": yb, "g": [], "l": []}, [])
 
 
+def ghost_jet_loss_grad(flat, arch, act, pts, target_du, vel_w, coef):
+    """Opt-in C^1 interface extension (NOT in the reference, whose ghost
+    coupling matches values only, worker.py:179-197): (sq, grad) of
+    coef * sum_n sum_i sum_c w_c (d u_c/d x_i - target_du[n, i, c])^2, first
+    derivatives of the velocity w.r.t. every input, through the same jet
+    forward / reverse sweep as the PDE head (tape.py:22-124)."""
+    pts = np.asarray(pts, dtype=np.float64)
+    n_in, nv = target_du.shape[1], target_du.shape[2]
+    Y, cache = jet_forward(flat, arch, act, pts, [])
+    w = np.ones(nv) if vel_w is None else np.asarray(vel_w, dtype=np.float64)
+    sq = 0.0
+    gb = []
+    for i in range(n_in):
+        d = Y["g"][i][:, :nv] - target_du[:, i, :]
+        sq += float(sum(w[c] * np.dot(d[:, c], d[:, c]) for c in range(nv)))
+        b = np.zeros_like(Y["g"][i])
+        b[:, :nv] = 2.0 * coef * w * d
+        gb.append(b)
+    return sq, jet_backward(flat, arch, act, cache, {"v": np.zeros_like(Y["v"]), "g": gb, "l": []}, [])
+
+
 # ----------------------------------------------------------------------------
 # per-rank objective, optimiser, exchange, serial loop
 # ----------------------------------------------------------------------------

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("FLOWREC_B200_LIB") or os.path.join(HERE, "_lib", "lib
 ACT_TANH, ACT_SIN = 0, 1
 STEADY2D, UNSTEADY2D, UNSTEADY3D = 0, 1, 2
 F32, F64 = 0, 1
-MODE_PDE, MODE_MSE, MODE_VALUE, MODE_JET = 0, 1, 2, 3
+MODE_PDE, MODE_MSE, MODE_VALUE, MODE_JET, MODE_GJ = 0, 1, 2, 3, 4
 FLAG_NONFINITE_LOSS, FLAG_NONFINITE_GRAD, FLAG_EXCHANGE_TIMEOUT = 1, 2, 4
 
 REGIME_CODES = {"steady2d": STEADY2D, "unsteady2d": UNSTEADY2D, "unsteady3d": UNSTEADY3D}
@@ -92,6 +92,7 @@ _SIGS = {
     "fr_epoch_fwd_bwd_gated": [_P, _P, _P, C.c_longlong, C.c_double, C.POINTER(MseSet), C.c_int, _P, _P,
                                C.POINTER(C.c_void_p), _P, C.POINTER(EpochGate), _P],
     "fr_signal": [_P, C.c_uint, C.c_uint, _P],
+    "fr_ghost_jet_fwd_bwd": [_P, _P, _P, _P, C.c_longlong, _P, C.c_double, _P, _P, _P, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
@@ -138,7 +139,7 @@ def lib():
 # functions that enqueue kernels (counted for the bench's gpu_launches claim)
 LAUNCHERS = frozenset({
     "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_epoch_fwd_bwd_gated",
-    "fr_signal", "fr_value_fwd", "fr_jet_fwd",
+    "fr_signal", "fr_ghost_jet_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_jet_act_forward",
     "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
 })

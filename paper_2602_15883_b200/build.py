@@ -20,7 +20,7 @@ LIB = os.path.join(OUT_DIR, "libflowrec_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 SOURCES = (["capi.cu", "wide_f32.cu", "wide_f64.cu", "tc_probe.cu", "tcwide_f32.cu"]
-           + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet") for d in ("f32", "f64")])
+           + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet", "gj") for d in ("f32", "f64")])
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -21,6 +21,7 @@ FR_DECL(mode_entry_PDE)
 FR_DECL(mode_entry_MSE)
 FR_DECL(mode_entry_VALUE)
 FR_DECL(mode_entry_JET)
+FR_DECL(mode_entry_GJ)
 #undef FR_DECL
 int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
 int wide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
@@ -240,6 +241,9 @@ static int mode_call(const fr_plan* p, int mode, const KArgs* a, int grid, cudaS
     case FR_MODE_JET:
       r = f32 ? mode_entry_JET_f32(act, reg, w, a, grid, st, info, L) : mode_entry_JET_f64(act, reg, w, a, grid, st, info, L);
       break;
+    case FR_MODE_GJ:
+      r = f32 ? mode_entry_GJ_f32(act, reg, w, a, grid, st, info, L) : mode_entry_GJ_f64(act, reg, w, a, grid, st, info, L);
+      break;
     default: return fail("unknown mode %d", mode);
   }
   if (r == -1) return fail("kernel variant not compiled (mode %d dtype %d act %d regime %d width %d)", mode, I.dtype, I.act, I.regime, I.width_pad);
@@ -286,7 +290,7 @@ static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WIn
   const long long L = I.hidden_layers, WP = I.width_pad;
   z->ntiles = (n + wi->ppt - 1) / wi->ppt;
   z->act = L * z->ntiles * WP * wi->rows;
-  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
   // SIMT: activation stash; tensor cores: row-quad-major S_l and Zbar_l copies
   z->stash = !bwd ? 0
              : is_tc(p, mode) ? 2 * L * z->ntiles * WP * 128
@@ -307,7 +311,7 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
     WideSizes z;
     WInfo wi{};
     if (wide_sizes(p, mode, n, &z, &wi)) return 1;
-    const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+    const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
     const size_t esz = p->info.dtype == FR_F32 ? 4 : 8;
     const int ks = wide_ks(p, mode);
     out->grid = ks;
@@ -331,7 +335,7 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
   out->threads = ki.nt;
   out->points_per_tile = ki.ppt;
   out->jet_streams = 1 + 2 * I.n_in;
-  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
   out->gpart_elems = bwd ? (long long)out->grid * I.np_pad : 0;
   out->lpart_elems = bwd ? (long long)out->grid * 2 : 0;
   const size_t esz = I.dtype == FR_F32 ? 4 : 8;
@@ -359,7 +363,7 @@ static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* 
   }
   auto al = [](long long e) { return (e + 63) / 64 * 64; };
   char* base = static_cast<char*>(scratch);
-  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE);
+  const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
   a.act = base;
   base += al(z.act) * esz;
   if (bwd) {
@@ -587,6 +591,22 @@ extern "C" int fr_signal(unsigned* word, unsigned value, unsigned delay_ns, fr_s
   ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_signal");
   return 0;
+}
+
+extern "C" int fr_ghost_jet_fwd_bwd(const fr_plan* p, const void* kparams, const void* pts, const void* target_du,
+                                    long long n, const double* vel_w, double coef, double* gpart, double* lpart,
+                                    void* scratch, fr_stream_t stream) {
+  if (!p || !kparams || (n > 0 && (!pts || !target_du || !gpart || !lpart || !scratch)))
+    return fail("fr_ghost_jet_fwd_bwd: NULL argument");
+  if (n < 0) return fail("fr_ghost_jet_fwd_bwd: negative point count");
+  if (is_wide(p)) return fail("fr_ghost_jet_fwd_bwd: hidden width > 64 is not supported by the extension");
+  KArgs a{};
+  a.kp = kparams; a.pts = pts; a.tu = target_du; a.gpart = gpart; a.lpart = lpart; a.scratch = scratch;
+  a.coef = coef;
+  for (int c = 0; c < 4; ++c) a.velw[c] = 1.0;
+  if (vel_w)
+    for (int c = 0; c < p->info.n_vel; ++c) a.velw[c] = vel_w[c];
+  return launch_train(p, FR_MODE_GJ, a, n, stream);
 }
 
 extern "C" int fr_value_fwd(const fr_plan* p, const void* kparams, const void* pts, long long n, void* out,

@@ -38,7 +38,7 @@ extern long long g_kernel_launches;
 
 enum { ACT_TANH = 0, ACT_SIN = 1 };
 enum { REG_STEADY2D = 0, REG_UNSTEADY2D = 1, REG_UNSTEADY3D = 2 };
-enum { MODE_PDE = 0, MODE_MSE = 1, MODE_VALUE = 2, MODE_JET = 3 };
+enum { MODE_PDE = 0, MODE_MSE = 1, MODE_VALUE = 2, MODE_JET = 3, MODE_GJ = 4 };
 
 // Input layout (t,)x,y[,z]; outputs velocity + p (physics.py:17-67).
 template <int REG> struct Regime;
@@ -55,12 +55,14 @@ template <> struct Regime<REG_UNSTEADY3D> {
 // Jet streams carried per point.  PDE mode drops the reference's d2/dt2 block
 // (computed at builders.py:95 but never read by the residual, physics.py:89;
 // its adjoint is identically zero).  JET mode (predict_jet) keeps every block.
+// GJ mode (ghost-derivative matching, the opt-in C^1 interface extension)
+// carries value + first derivatives only.
 template <int MODE, int REG> struct Streams {
   using R = Regime<REG>;
-  static constexpr bool JET = (MODE == MODE_PDE || MODE == MODE_JET);
+  static constexpr bool JET = (MODE == MODE_PDE || MODE == MODE_JET || MODE == MODE_GJ);
   static constexpr int NG = JET ? R::DIN : 0;
   static constexpr int LAP0 = (MODE == MODE_PDE) ? R::HAS_T : 0;
-  static constexpr int NL = JET ? (R::DIN - LAP0) : 0;
+  static constexpr int NL = (JET && MODE != MODE_GJ) ? (R::DIN - LAP0) : 0;
   static constexpr int S = 1 + NG + NL;
   // rows owned by one thread: all streams of one point (jet modes) so the
   // activation jet is register-local, or 6 independent points (value modes).
@@ -72,7 +74,7 @@ constexpr int FLAG_EXCHANGE_TIMEOUT = 4;  // == FR_FLAG_EXCHANGE_TIMEOUT (flowre
 struct KArgs {
   const void* kp;       // kernel params (T), padded layout, see ParamLayout
   const void* pts;      // (n, DIN) T
-  const void* tu;       // MSE: (n, NVEL) T
+  const void* tu;       // MSE: (n, NVEL) T ; GJ: (n, DIN, NVEL) T derivative targets
   const void* tp;       // MSE: (n,) T or null
   void* out;            // VALUE: (n, NOUT) T ; JET: (n, S, NOUT) T
   double* gpart;        // [gridDim.x][np_pad] gradient partials

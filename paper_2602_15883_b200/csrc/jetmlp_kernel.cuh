@@ -122,7 +122,7 @@ struct JetCfg {
   static constexpr int DIN = R::DIN, NOUT = R::NOUT, NVEL = R::NVEL, HAS_T = R::HAS_T;
   static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0, RPT = St::RPT;
   static constexpr bool JET = St::JET;
-  static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE);
+  static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE || MODE == MODE_GJ);
   // 12 warps per SM where the FP32 tile buffers still fit (W = 64, <= 6 streams);
   // otherwise 8 (FP32) or 4 (FP64 parity build)
   static constexpr int NT_DEFAULT = sizeof(T) == 4 ? ((W == 64 && St::RPT <= 6) ? 384 : 256) : 128;
@@ -762,6 +762,28 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           for (int k = 0; k < NVEL; ++k) yb[GRAD(TOFF + k) * NOUT + k] += rb;
         }
       }
+    } else if constexpr (MODE == MODE_GJ) {
+      // C^1 interface extension (off by default; the reference couples values
+      // only, worker.py:179-197): sum_i sum_c w_c (d u_c/d x_i - target)^2
+      const T two_c = T(2.0 * a.coef);
+      for (int pt = tid; pt < PPT; pt += NT) {
+        T* yb = Ybs + pt * S * NOUT;
+#pragma unroll
+        for (int i = 0; i < S * NOUT; ++i) yb[i] = T(0);
+        if (pt >= rem) continue;
+        const T* y = Ys + pt * S * NOUT;
+        const T* td = static_cast<const T*>(a.tu) + (p0 + pt) * (NG * NVEL);
+        double sq = 0.0;
+#pragma unroll
+        for (int i = 0; i < NG; ++i)
+#pragma unroll
+          for (int c = 0; c < NVEL; ++c) {
+            const T d = y[(1 + i) * NOUT + c] - __ldcg(td + i * NVEL + c);
+            sq += a.velw[c] * (double(d) * double(d));
+            yb[(1 + i) * NOUT + c] = (two_c * T(a.velw[c])) * d;
+          }
+        lacc0 += sq;
+      }
     } else {  // MODE_MSE: squared error against targets (builders.py:103-141)
       const T two_vc = T(2.0 * a.coef);
       const T two_pc = T(2.0 * a.pcoef);
@@ -889,7 +911,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
 #pragma unroll
               for (int i = 0; i < NG; ++i) {
                 T t = sb[1 + i][j] * d1;
-                if (i >= LAP0) t += (T(2) * ga[i]) * sb[1 + NG + (i - LAP0)][j];
+                if (i >= LAP0 && i - LAP0 < NL) t += (T(2) * ga[i]) * sb[1 + NG + (i - LAP0)][j];
                 zb[1 + i][j] = t;
               }
 #pragma unroll
@@ -1042,7 +1064,19 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           // slice of the 64x64 block over rs = 0, 1, ... (fixed order) and
           // red.adds it once
           auto kidx = [&](int x) { return x < 4 ? 4 * kt + x : 4 * (kt + KT) + (x - 4); };
-          if (active) {
+          static_assert(RSPLIT == 1 || RSPLIT * W * W <= C::XELEMS, "dW row-range partials must fit in Xs");
+          if constexpr (RSPLIT == 1) {
+            // one row range: every dW element has exactly one owner thread,
+            // which red.adds its 8x8 block straight from registers
+            if (active) {
+              double* dst = gp + pl.off_w(l);
+#pragma unroll
+              for (int x = 0; x < 8; ++x)
+#pragma unroll
+                for (int y = 0; y < 8; ++y)
+                  red_add(dst + kidx(x) * W + (y < 4 ? 4 * ut + y : 4 * (ut + KT) + (y - 4)), double(acc[x][y]));
+            }
+          } else if (active) {
             T* dst = Xs + rs * W * W;
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
@@ -1058,7 +1092,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
             for (int h = 1; h < NT / W; ++h) sb += Dbs[h * W + tid];
             red_add(gp + pl.off_b(l) + tid, double(sb));
           }
-          {
+          if constexpr (RSPLIT > 1) {
             double* dst = gp + pl.off_w(l);
             for (int e = tid; e < W * W; e += NT) {
               T sum = Xs[e];
@@ -1123,7 +1157,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
 #pragma unroll
             for (int i = 0; i < NG; ++i) {
               T t = sb[1 + i][j] * d1;
-              if (i >= LAP0) t += (T(2) * d2) * zg[i] * sb[1 + NG + (i - LAP0)][j];
+              if (i >= LAP0 && i - LAP0 < NL) t += (T(2) * d2) * zg[i] * sb[1 + NG + (i - LAP0)][j];
               zb[1 + i][j] = t;
             }
 #pragma unroll

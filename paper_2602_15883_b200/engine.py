@@ -172,6 +172,23 @@ def pde_loss_grad(plan, flat, points, coef):
     return sq, g
 
 
+def ghost_jet_loss_grad(plan, flat, points, target_du, vel_w, coef):
+    """(sq, gradient of coef * sq) of the opt-in ghost-derivative head:
+    sq = sum_n sum_i sum_c w_c (d u_c / d x_i - target_du[n, i, c])^2."""
+    kp = _kparams_for(plan, flat)
+    pts = to_device(np.atleast_2d(points), plan.tdtype, plan.device)
+    td = to_device(target_du, plan.tdtype, plan.device)
+    n = pts.shape[0]
+    vw = (C.c_double * 4)(*(list(vel_w) + [1.0] * (4 - len(vel_w))))
+
+    def launch(gp, lp, sc):
+        X.call("fr_ghost_jet_fwd_bwd", plan.h, X.ptr(kp), X.ptr(pts), X.ptr(td), n, vw, float(coef), X.ptr(gp),
+               X.ptr(lp), X.ptr(sc), X.stream_ptr())
+
+    sq, _, g = _train_call(plan, X.MODE_GJ, n, launch)
+    return sq, g
+
+
 def mse_loss_grad(plan, flat, points, target_u, target_p, vel_w, vel_coef, p_coef):
     """(sq_u, sq_p, gradient) of the MSE head; target_p None omits the p term."""
     kp = _kparams_for(plan, flat)

@@ -132,16 +132,17 @@ class LocalTrainer:
         for r in self.order:
             w = self.workers[r]
             for k, (edge, _, _, _) in enumerate(w.edges):
-                tu, tp = self.workers[edge.dest].objective.target_slice(edge.ghost_index)
-                self.routes.append((w, k, tu, tp))
+                dobj = self.workers[edge.dest].objective
+                tu, tp = dobj.target_slice(edge.ghost_index)
+                self.routes.append((w, k, tu, tp, dobj.target_du_slice(edge.ghost_index)))
         self.graphs = {}
         self._ran_eager = False
 
     def enqueue_exchange(self):
         for r in self.order:
             self.workers[r].produce()
-        for w, k, tu, tp in self.routes:
-            w.pack_edge(k, tu, tp)
+        for w, k, tu, tp, tdu in self.routes:
+            w.pack_edge(k, tu, tp, out_du=tdu)
         for w in self.workers.values():
             w.objective.mark_targets_set()
 
@@ -164,8 +165,8 @@ class LocalTrainer:
         cur = torch.cuda.current_stream()
         self.comm.wait_stream(cur)
         with torch.cuda.stream(self.comm):
-            for w, k, tu, tp in self.routes:
-                w.pack_edge(k, tu, tp, stream=self.comm)
+            for w, k, tu, tp, tdu in self.routes:
+                w.pack_edge(k, tu, tp, stream=self.comm, out_du=tdu)
             for i, r in enumerate(self.order):
                 X.call("fr_signal", C.c_void_p(self.gates[i].data_ptr()), 1, self.signal_delay_ns,
                        X.stream_ptr(self.comm))
@@ -265,17 +266,16 @@ def p2p_routes(plan: TrainingPlan, rank: int):
 def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
     """Issue every send/recv of one round as a single batched P2P group.
 
-    send_bufs[k] / recv_bufs[gi] are (u, p) tensor pairs.  Returns the work
+    send_bufs[k] / recv_bufs[gi] are (u, p) tensor pairs, or (u, p, du) with
+    the derivative-coupling extension.  Returns the work
     handles; waiting on them orders the caller's stream after the transfers."""
     import torch.distributed as dist
 
     ops = []
     for dest, k, _ in sends:
-        u, p = send_bufs[k]
-        ops += [dist.P2POp(dist.isend, u, dest, group), dist.P2POp(dist.isend, p, dest, group)]
+        ops += [dist.P2POp(dist.isend, t, dest, group) for t in send_bufs[k]]
     for src, gi, _ in recvs:
-        u, p = recv_bufs[gi]
-        ops += [dist.P2POp(dist.irecv, u, src, group), dist.P2POp(dist.irecv, p, src, group)]
+        ops += [dist.P2POp(dist.irecv, t, src, group) for t in recv_bufs[gi]]
     return dist.batch_isend_irecv(ops) if ops else []
 
 
@@ -309,14 +309,22 @@ class DistributedTrainer:
         self.worker = w = RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas)
         self.sends, self.recvs = p2p_routes(plan, self.rank)
         nv, T, dev = plan.regime.n_vel, w.plan.tdtype, w.plan.device
+        nin = plan.regime.n_inputs
         self.send_bufs = [(torch.empty((n, nv), dtype=T, device=dev), torch.empty(n, dtype=T, device=dev))
+                          + ((torch.empty((n, nin, nv), dtype=T, device=dev),) if w.send_derivatives else ())
                           for _, _, n in self.sends]
-        self.recv_bufs = {gi: w.objective.target_slice(gi) for _, gi, _ in self.recvs}
+        self.recv_bufs = {gi: w.objective.target_slice(gi)
+                          + ((w.objective.target_du_slice(gi),) if w.send_derivatives else ())
+                          for _, gi, _ in self.recvs}
         self._connected = False
         if self.overlap:
             self.comm = torch.cuda.Stream()
             self.gate_word = torch.zeros(1, dtype=torch.int32, device=dev)
             self.gate = w.objective.make_gate(self.gate_word, w.flags)
+
+    def _du(self, k):
+        b = self.send_bufs[k]
+        return b[2] if len(b) > 2 else None
 
     def epoch(self, e):
         """Exchange (if due) then the fused epoch (overlapped, see the class doc)."""
@@ -336,7 +344,7 @@ class DistributedTrainer:
                 with torch.cuda.stream(self.comm):
                     w.produce(stream=self.comm)
                     for k, _ in enumerate(self.sends):
-                        w.pack_edge(k, *self.send_bufs[k], stream=self.comm)
+                        w.pack_edge(k, *self.send_bufs[k][:2], stream=self.comm, out_du=self._du(k))
                     for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                         wk.wait()  # transport stream waits for the transfers
                     X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
@@ -349,7 +357,7 @@ class DistributedTrainer:
             if exchange:
                 w.produce()
                 for k, _ in enumerate(self.sends):
-                    w.pack_edge(k, *self.send_bufs[k])
+                    w.pack_edge(k, *self.send_bufs[k][:2], out_du=self._du(k))
                 for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                     wk.wait()  # orders the compute stream after the transfers (no host sync)
                 self._connected = True

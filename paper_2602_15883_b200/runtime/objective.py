@@ -29,9 +29,14 @@ KINDS = ("spatial", "temporal")
 class DeviceObjective:
     """Resident datasets, workspaces and the per-epoch launch sequence."""
 
-    def __init__(self, plan, regime, datasets, weights, max_ctas=0):
+    def __init__(self, plan, regime, datasets, weights, max_ctas=0, ghost_derivative_weight=0.0):
         self.plan = plan
         self.max_ctas = int(max_ctas)  # persistent-grid cap (SMs left free for the exchange transport)
+        # opt-in C^1 interface extension (0: the reference's value-only coupling)
+        self.gd_weight = float(ghost_derivative_weight)
+        if self.gd_weight < 0:
+            raise ValueError("ghost derivative weight must be non-negative")
+        self.gd_launches = []
         self.regime = regime
         self.weights = weights
         dev, T = plan.device, plan.tdtype
@@ -86,6 +91,8 @@ class DeviceObjective:
             if counts[kind]:
                 self.set_order.append((seg, kind))
         self.wide = plan.info.width_pad > 64
+        if self.wide and self.gd_weight > 0:
+            raise ValueError("the ghost-derivative extension needs hidden width <= 64")
         if self.wide:
             self._init_wide(plan, counts, weights, dev)
             return
@@ -100,10 +107,10 @@ class DeviceObjective:
         self.seg_rows = (ctypes.c_int * 4)(*[ws.grid if sg in present else 0 for sg in range(4)])
         self.total_rows = ws.grid
         npad = plan.info.np_pad
-        self.gpart = torch.empty(ws.grid * npad, dtype=torch.float64, device=dev)
         self.lpart = torch.zeros(len(present) * ws.grid * 2, dtype=torch.float64, device=dev)
         block = {sg: self.lpart.data_ptr() + 8 * 2 * ws.grid * i for i, sg in enumerate(present)}
         self.lpart_blocks = (ctypes.c_void_p * 4)(block[SEG_PDE], *[block[sg] for sg, _ in self.set_order])
+        self._init_ghost_derivatives(plan, ws.grid, npad, dev)
         self.scratch = torch.empty(max(ws.scratch_bytes, 16), dtype=torch.uint8, device=dev)
         self.sets = (X.MseSet * 3)()
         for i, (sg, kind) in enumerate(self.set_order):
@@ -120,6 +127,31 @@ class DeviceObjective:
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
         # ghost sets follow obs in set_order: the overlapped exchange gates them
         self.first_ghost_set = 1 if self.n_obs else 0
+
+    def _init_ghost_derivatives(self, plan, epoch_rows, npad, dev):
+        """Extension buffers: per ghost kind the derivative targets (N, n_in,
+        n_vel) and one FR_MODE_GJ launch whose gradient-partial rows follow the
+        epoch kernel's in `gpart` (so fr_reduce_grad folds them in)."""
+        self.gd_launches = []
+        self.gpart = None
+        rows = epoch_rows
+        if self.gd_weight > 0 and self.ghost:
+            n_in, nv = self.regime.n_inputs, self.regime.n_vel
+            lrow = 0
+            for kind, g in self.ghost.items():
+                n = g["pts"].shape[0]
+                g["tdu"] = torch.zeros((n, n_in, nv), dtype=plan.tdtype, device=dev)
+                ws = plan.workspace(X.MODE_GJ, n)
+                self.gd_launches.append((kind, n, rows, lrow, ws))
+                rows += ws.grid
+                lrow += ws.loss_rows
+            self.gd_lpart = torch.zeros(max(lrow, 1) * 2, dtype=torch.float64, device=dev)
+            self.gd_rows = (ctypes.c_int * 1)(lrow)
+            self.gd_sums = torch.zeros(2, dtype=torch.float64, device=dev)
+            self.gd_scratch = torch.empty(max(max(w.scratch_bytes for *_, w in self.gd_launches), 16),
+                                          dtype=torch.uint8, device=dev)
+        self.total_rows = rows
+        self.gpart = torch.empty(rows * npad, dtype=torch.float64, device=dev)
 
     def make_gate(self, gate_word, flags, timeout_ms=60000):
         """fr_epoch_gate for the overlapped exchange (ghost sets wait on gate_word)."""
@@ -182,11 +214,34 @@ class DeviceObjective:
         g = self.ghost[kind]
         return g["tu"][off : off + n], g["tp"][off : off + n]
 
+    def target_du_slice(self, gi):
+        """Device view (n, n_in, n_vel) of ghost set gi's derivative targets
+        (extension; None when ghost_derivative_weight == 0)."""
+        kind, off, n = self.ghost_slices[gi]
+        tdu = self.ghost[kind].get("tdu")
+        return None if tdu is None else tdu[off : off + n]
+
+    def ghost_derivative_loss(self):
+        """Unweighted extension term of the last epoch run with sums:
+        sum w_c (d u_c/d x_i - target)^2 / N_ghost_total (0 when disabled)."""
+        if not self.gd_launches:
+            return 0.0
+        return float(self.gd_sums[0].item()) / self.n_ghost_total
+
     def set_ghost_targets(self, values):
         """values aligned with datasets.ghosts: (u (g, n_vel), p (g,)) arrays/tensors."""
         nv = self.regime.n_vel
         for gi, (kind, off, n) in self.ghost_slices.items():
-            u, p = values[gi]
+            u, p = values[gi][0], values[gi][1]
+            du = values[gi][2] if len(values[gi]) > 2 else None
+            tdu = self.target_du_slice(gi)
+            if tdu is not None:
+                if du is None:
+                    raise ValueError("ghost derivative coupling is on: messages must carry derivatives")
+                du_t = du if torch.is_tensor(du) else torch.as_tensor(np.asarray(du, dtype=np.float64))
+                if tuple(du_t.shape) != tuple(tdu.shape):
+                    raise ValueError("ghost derivative target shape mismatch")
+                tdu.copy_(du_t)
             u_t = u if torch.is_tensor(u) else torch.as_tensor(np.asarray(u, dtype=np.float64))
             p_t = p if torch.is_tensor(p) else torch.as_tensor(np.asarray(p, dtype=np.float64))
             if tuple(u_t.shape) != (n, nv) or tuple(p_t.shape) != (n,):
@@ -227,8 +282,16 @@ class DeviceObjective:
                    self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
                    X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch),
                    ctypes.byref(gate) if gate is not None else None, st)
+        npad = plan.info.np_pad
+        for kind, n, grow, lrow, _ in self.gd_launches:
+            g = self.ghost[kind]
+            X.call("fr_ghost_jet_fwd_bwd", plan.h, X.ptr(kparams), X.ptr(g["pts"]), X.ptr(g["tdu"]), n, self.vel_w,
+                   self.gd_weight / self.n_ghost_total, self.gpart.data_ptr() + 8 * grow * npad,
+                   self.gd_lpart.data_ptr() + 16 * lrow, X.ptr(self.gd_scratch), st)
         X.call("fr_reduce_grad", plan.h, X.ptr(self.gpart), self.total_rows, X.ptr(self.grad), 0,
                X.ptr(self.norm_parts), st)
+        if with_sums and self.gd_launches:
+            X.call("fr_reduce_loss", X.ptr(self.gd_lpart), self.gd_rows, 1, X.ptr(self.gd_sums), st)
         if with_sums:
             X.call("fr_reduce_loss", X.ptr(self.lpart), self.seg_rows, 4, X.ptr(self.sums), st)
 
@@ -253,7 +316,8 @@ class LocalObjective:
     is a float64 numpy vector in the reference's flat layout.
     """
 
-    def __init__(self, config, regime, datasets, weights, batch_size, dtype="float32", math=None):
+    def __init__(self, config, regime, datasets, weights, batch_size, dtype="float32", math=None,
+                 ghost_derivative_weight=0.0):
         if batch_size < 1:
             raise ValueError("batch size must be >= 1")
         self.config = config
@@ -261,7 +325,8 @@ class LocalObjective:
         self.weights = weights
         self.batch = int(batch_size)
         self.plan = get_plan(config, regime.kind, regime.reynolds, dtype, math)
-        self.dev = DeviceObjective(self.plan, regime, datasets, weights)
+        self.dev = DeviceObjective(self.plan, regime, datasets, weights,
+                                   ghost_derivative_weight=ghost_derivative_weight)
         self.n_obs, self.n_colloc = self.dev.n_obs, self.dev.n_colloc
         self.n_ghost, self.n_ghost_total = self.dev.n_ghost, self.dev.n_ghost_total
         self.n_params = config.n_params
@@ -283,6 +348,8 @@ class LocalObjective:
             grad_out = np.zeros(self.n_params)
         grad_out += grad
         total = compose_loss(parts, self.weights)
+        if self.dev.gd_launches:  # opt-in C^1 extension term
+            total += self.dev.gd_weight * self.dev.ghost_derivative_loss()
         if not np.isfinite(total):
             raise FloatingPointError(
                 f"non-finite training loss: obs={parts.obs} pde={parts.pde} ghost_u={parts.ghost_u} "

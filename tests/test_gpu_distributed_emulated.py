@@ -47,9 +47,8 @@ class CopyTransport:
             k = next(k for k, e in enumerate(self.plan.worker_specs[src].outgoing)
                      if e.dest == me and e.ghost_index == gi)
             cur.wait_event(self.packed[src])
-            u, p = recv_bufs[gi]
-            u.copy_(peer.send_bufs[k][0], non_blocking=True)
-            p.copy_(peer.send_bufs[k][1], non_blocking=True)
+            for dst, srcbuf in zip(recv_bufs[gi], peer.send_bufs[k]):
+                dst.copy_(srcbuf, non_blocking=True)
         done = torch.cuda.Event()
         done.record(cur)
         self.taken[me] = done
