@@ -115,3 +115,24 @@ def test_distributed_trainer_matches_in_process(golden, tag, overlap, monkeypatc
         assert used_overlap == overlap
         assert np.array_equal(flat, w.flat.cpu().numpy()), r
         assert np.array_equal(hist[:, 1:], np.array(w.history)[:, 1:]), r
+
+
+def test_distributed_trainer_with_derivative_coupling(golden, monkeypatch):
+    """The (u, p, du) messages of the C^1 extension move through the same P2P
+    path: overlapped distributed trainer == in-process trainer, bit for bit."""
+    import dataclasses
+
+    from paper_2602_15883_b200.runtime import build_plan
+    from paper_2602_15883_b200.runtime.driver import LocalTrainer
+
+    pb, plan0 = training_plan("p8", golden)
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config,
+                      dataclasses.replace(plan0.train_config, ghost_derivative_weight=0.5))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ref = LocalTrainer(plan, reserve_sms=sms - MAX_CTAS)
+    ref.run(plan.train_config.epochs)
+    got = _run_distributed(plan, True, monkeypatch)
+    for r, w in ref.workers.items():
+        w.sync_history()
+        assert np.array_equal(got[r][0], w.flat.cpu().numpy()), r
+        assert np.array_equal(got[r][1][:, 1:], np.array(w.history)[:, 1:]), r
