@@ -69,6 +69,7 @@ typedef struct {
   size_t smem_bytes;
   int loss_rows;           /* rows of 2 doubles in lpart (== grid for the fused kernels) */
   int wide;                /* 1: layer-wise SIMT wide kernels (hidden width > 64), 2: TF32 tcgen05 wide kernels */
+  long long tiles;         /* work tiles of the launch (persistent kernels deal them round robin) */
 } fr_workspace;
 
 /* Plan: validated network + regime description (replaces per-bind checks). */

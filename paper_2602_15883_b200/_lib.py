@@ -42,7 +42,7 @@ class Workspace(C.Structure):
         ("jet_streams", C.c_int),
         ("gpart_elems", C.c_longlong), ("lpart_elems", C.c_longlong),
         ("scratch_bytes", C.c_longlong), ("smem_bytes", C.c_size_t),
-        ("loss_rows", C.c_int), ("wide", C.c_int),
+        ("loss_rows", C.c_int), ("wide", C.c_int), ("tiles", C.c_longlong),
     ]
 
 

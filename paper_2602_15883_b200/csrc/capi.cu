@@ -324,6 +324,7 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
     out->scratch_bytes = z.total * (long long)esz;
     out->smem_bytes = 0;
     out->wide = is_tc(p, mode) ? 2 : 1;
+    out->tiles = z.ntiles;
     return 0;
   }
   KInfo ki{};
@@ -332,6 +333,7 @@ extern "C" int fr_plan_workspace(const fr_plan* p, int mode, long long n, fr_wor
   const long long ntiles = (n + ki.ppt - 1) / ki.ppt;
   const int sms = I.num_sms > 0 ? I.num_sms : 148;
   out->grid = int(ntiles < sms ? ntiles : sms);
+  out->tiles = ntiles;
   out->threads = ki.nt;
   out->points_per_tile = ki.ppt;
   out->jet_streams = 1 + 2 * I.n_in;
@@ -488,6 +490,7 @@ extern "C" int fr_epoch_workspace_capped(const fr_plan* p, long long n_colloc, c
   long long tiles = (n_colloc + ki.ppt - 1) / ki.ppt;
   for (int i = 0; i < n_set_count; ++i) tiles += (n_sets[i] + ki.ppt_mse - 1) / ki.ppt_mse;
   out->grid = int(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+  out->tiles = tiles;
   out->threads = ki.nt;
   out->points_per_tile = ki.ppt;
   out->jet_streams = 0;

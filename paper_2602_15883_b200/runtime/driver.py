@@ -97,6 +97,30 @@ def build_plan(subdomains, datasets, expert_config: ExpertConfig, train_config: 
 # -- in-process (single GPU, all ranks) ---------------------------------------------
 
 
+def _free_sms_without_extra_wave(plan, ws, most=2):
+    """SMs the overlapped exchange may keep free (up to `most`) without adding
+    a wave of tiles to this rank's persistent epoch kernel; 0 if even one
+    would (the exchange then runs in stream order on the full grid)."""
+    from ..engine import get_plan
+
+    tc = plan.train_config
+    ep = get_plan(plan.expert_config, plan.regime.kind, plan.regime.reynolds, "float32", tc.math)
+    d = ws.datasets
+    per_kind = {}
+    for g in d.ghosts:
+        per_kind[g.kind] = per_kind.get(g.kind, 0) + g.points.shape[0]
+    sets = ([d.n_obs] if d.n_obs else []) + [per_kind[k] for k in ("spatial", "temporal") if k in per_kind]
+    n_sets = (C.c_longlong * 3)(*(sets + [0] * 3)[:3])
+    wsp = X.Workspace()
+    X.call("fr_epoch_workspace", ep.h, d.n_colloc, n_sets, len(sets), C.byref(wsp))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    waves = -(-wsp.tiles // sms)
+    for r in range(most, 0, -1):
+        if -(-wsp.tiles // (sms - r)) == waves:
+            return r
+    return 0
+
+
 def _overlap_max_ctas(reserve_sms):
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     return max(1, sms - int(reserve_sms))
@@ -282,20 +306,22 @@ def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
 class DistributedTrainer:
     """This process's rank of a torch.distributed group (NCCL over NVLink).
 
-    overlap=True (default for the fused small-width kernel): the whole ghost
-    round is overlapped with the interior work.  The producer (value forward
-    of the neighbours' ghost points), the pack and the NCCL send/recv group all
-    run on a transport stream which, once the receives have landed, sets this
-    rank's gate word (fr_signal).  The epoch kernel is launched at once on the
-    compute stream with its persistent grid capped `reserve_sms` below the SM
-    count (so the producer's and NCCL's kernels have SMs to run on); every CTA
-    walks its PDE and observation tiles first and only its ghost tiles wait on
-    the gate, so producer + transfer hide under the interior residual work.
-    The optimiser waits for the transport stream (the producer read the
-    pre-update parameters).  The first exchange runs in stream order (it also
-    brings up the NCCL connections, which may synchronise the device)."""
+    overlap=True (default for the fused small-width kernel): the ghost
+    transfer is overlapped with the interior work.  The producer (value
+    forward of the neighbours' ghost points) and the pack run on the compute
+    stream (~20 us); the NCCL send/recv group then runs on a transport stream
+    which, once the receives have landed, sets this rank's gate word
+    (fr_signal).  The epoch kernel is launched at once with its persistent grid
+    capped `reserve_sms` below the SM count, so NCCL's kernels have an SM to run
+    on; every CTA walks its PDE and observation tiles first and only its ghost
+    tiles wait on the gate.  By default the reserve is the largest of 2, 1 SMs
+    that does not add a wave of tiles to the kernel (P=8: 1319 tiles, 147 CTAs
+    keep 9 per CTA where 146 would need 10); if even one SM would, the exchange
+    runs in stream order on the full grid.  The first exchange always runs in
+    stream order (it also brings up the NCCL connections, which may
+    synchronise the device)."""
 
-    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=2):
+    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=None):
         import torch.distributed as dist
 
         self.plan = plan
@@ -305,7 +331,14 @@ class DistributedTrainer:
         ws = plan.worker_specs[self.rank]
         wide = max(plan.expert_config.arch[1:-1], default=0) > 64
         self.overlap = bool(overlap) and not wide and len(ws.datasets.ghosts) > 0
-        max_ctas = _overlap_max_ctas(reserve_sms) if self.overlap else 0
+        max_ctas = 0
+        if self.overlap:
+            if reserve_sms is None:
+                reserve_sms = _free_sms_without_extra_wave(plan, ws)
+            if reserve_sms > 0:
+                max_ctas = _overlap_max_ctas(reserve_sms)
+            else:
+                self.overlap = False  # reserving an SM would cost a whole extra tile wave
         self.worker = w = RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas)
         self.sends, self.recvs = p2p_routes(plan, self.rank)
         nv, T, dev = plan.regime.n_vel, w.plan.tdtype, w.plan.device
@@ -332,27 +365,23 @@ class DistributedTrainer:
         exchange = e % self.plan.train_config.comm_interval == 0
         cur = torch.cuda.current_stream()
         if exchange and self.overlap and self._connected:
-            # the epoch kernel is enqueued first so that it takes its capped
-            # grid; the producer and NCCL then run on the reserved SMs
+            # producer + pack on the compute stream (~20 us on the full GPU);
+            # the NCCL group and the gate signal on the transport stream, on the
+            # reserved SM(s), while the epoch kernel walks its interior tiles
+            w.produce()
+            for k, _ in enumerate(self.sends):
+                w.pack_edge(k, *self.send_bufs[k][:2], out_du=self._du(k))
             self.gate_word.zero_()
             ready = torch.cuda.Event()
-            ready.record(cur)  # parameters after the previous update; gate reset
+            ready.record(cur)
             w.objective.mark_targets_set()
-
-            def transport():
-                self.comm.wait_event(ready)
-                with torch.cuda.stream(self.comm):
-                    w.produce(stream=self.comm)
-                    for k, _ in enumerate(self.sends):
-                        w.pack_edge(k, *self.send_bufs[k][:2], stream=self.comm, out_du=self._du(k))
-                    for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
-                        wk.wait()  # transport stream waits for the transfers
-                    X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
-                # the optimiser rewrites the parameters the producer read, and the
-                # next round reuses the send buffers and targets
-                cur.wait_stream(self.comm)
-
-            w.enqueue_epoch(gate=self.gate, before_update=transport)
+            self.comm.wait_event(ready)
+            with torch.cuda.stream(self.comm):
+                for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                    wk.wait()  # transport stream waits for the transfers
+                X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
+            # the next round reuses the send buffers and targets
+            w.enqueue_epoch(gate=self.gate, before_update=lambda: cur.wait_stream(self.comm))
         else:
             if exchange:
                 w.produce()

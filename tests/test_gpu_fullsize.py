@@ -113,3 +113,21 @@ def test_p8_full_size_partition_covers_every_point():
     pb = cylinder2d_problem(n_procs=8, n_pde=500_000, hidden_layers=4, width=64, activation="tanh")
     sizes = [pb.datasets[r].colloc_points.shape[0] for r in range(8)]
     assert sum(sizes) == 500_000 and max(sizes) - min(sizes) <= 1
+
+
+def test_p8_overlap_reserve_keeps_the_wave_count():
+    """The overlapped exchange keeps SMs free only if the persistent kernel
+    needs no extra tile wave: P=8 rank 0 has 1,303 PDE + 16 MSE tiles, so one
+    SM (147 CTAs -> 9 tiles each), not two (146 -> 10)."""
+    import torch
+
+    from paper_2602_15883_b200.config import cylinder2d_problem
+    from paper_2602_15883_b200.runtime import TrainConfig, build_plan
+    from paper_2602_15883_b200.runtime.driver import _free_sms_without_extra_wave
+
+    pb = cylinder2d_problem(n_procs=8, n_pde=500_000, hidden_layers=4, width=64, activation="tanh")
+    tc = TrainConfig(epochs=2, batch_size=25000, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor)
+    plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("tile-wave arithmetic stated for 148 SMs")
+    assert _free_sms_without_extra_wave(plan, plan.worker_specs[0]) == 1
