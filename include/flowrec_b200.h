@@ -156,6 +156,20 @@ int fr_ghost_jet_fwd_bwd(const fr_plan* plan, const void* kparams, const void* p
                          long long n, const double* vel_w, double coef, double* gpart, double* lpart, void* scratch,
                          fr_stream_t stream);
 
+/* Ghost-exchange transport over NCCL point-to-point.  libnccl.so.2
+ * is resolved at run time (the copy a PyTorch process already holds).
+ * fr_nccl_get_unique_id writes 128 bytes on one rank; every rank passes them
+ * to fr_nccl_init.  fr_exchange enqueues one grouped round -- all sends and
+ * receives of this rank -- on `stream`; counts are elements of `dtype`
+ * (FR_F32 / FR_F64). */
+typedef struct fr_comm fr_comm;
+int fr_nccl_get_unique_id(void* id_out);
+int fr_nccl_init(const void* unique_id, int nranks, int rank, fr_comm** out);
+int fr_nccl_destroy(fr_comm* comm);
+int fr_exchange(fr_comm* comm, int n_send, const int* send_peers, const void* const* send_bufs,
+                const long long* send_counts, int n_recv, const int* recv_peers, void* const* recv_bufs,
+                const long long* recv_counts, int dtype, fr_stream_t stream);
+
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,
                  fr_stream_t stream);

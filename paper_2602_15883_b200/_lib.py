@@ -93,6 +93,11 @@ _SIGS = {
                                C.POINTER(C.c_void_p), _P, C.POINTER(EpochGate), _P],
     "fr_signal": [_P, C.c_uint, C.c_uint, _P],
     "fr_ghost_jet_fwd_bwd": [_P, _P, _P, _P, C.c_longlong, _P, C.c_double, _P, _P, _P, _P],
+    "fr_nccl_get_unique_id": [_P],
+    "fr_nccl_init": [_P, C.c_int, C.c_int, C.POINTER(_P)],
+    "fr_nccl_destroy": [_P],
+    "fr_exchange": [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(_P), C.POINTER(C.c_longlong), C.c_int,
+                    C.POINTER(C.c_int), C.POINTER(_P), C.POINTER(C.c_longlong), C.c_int, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],

@@ -19,7 +19,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflowrec_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = (["capi.cu", "wide_f32.cu", "wide_f64.cu", "tc_probe.cu", "tcwide_f32.cu"]
+SOURCES = (["capi.cu", "nccl_transport.cu", "wide_f32.cu", "wide_f64.cu", "tc_probe.cu", "tcwide_f32.cu"]
            + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet", "gj") for d in ("f32", "f64")])
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -74,7 +74,7 @@ def build(force=False, jobs=None, verbose=False, defines=(), lib=None):
             print(log, file=sys.stderr)
     tmp = lib + ".tmp"
     cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-           *[o for o, _ in results], "-o", tmp, "-lcudart"]
+           *[o for o, _ in results], "-o", tmp, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

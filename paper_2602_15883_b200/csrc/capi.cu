@@ -49,6 +49,13 @@ static int fail(const char* fmt, ...) {
   g_err = buf;
   return 1;
 }
+// error entry for the other translation units (nccl_transport.cu)
+namespace fr {
+int fail_msg(const char* msg) {
+  g_err = msg;
+  return 1;
+}
+}  // namespace fr
 static int cuda_fail(cudaError_t e, const char* where) {
   return fail("%s: CUDA error %d (%s)", where, int(e), cudaGetErrorString(e));
 }

@@ -303,6 +303,45 @@ def post_exchange(sends, recvs, send_bufs, recv_bufs, group=None):
     return dist.batch_isend_irecv(ops) if ops else []
 
 
+class FrNcclTransport:
+    """The library's own exchange transport (fr_nccl_init / fr_exchange, the C
+    ABI of SURVEY 8b): rank 0 makes the NCCL unique id, torch.distributed
+    broadcasts it once, and every exchange round is one grouped
+    ncclSend/ncclRecv set enqueued on the current stream."""
+
+    def __init__(self, dtype):
+        import torch.distributed as dist
+
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            X.call("fr_nccl_get_unique_id", uid)
+        box = [uid.raw]
+        dist.broadcast_object_list(box, src=0)
+        uid = C.create_string_buffer(box[0], 128)
+        self.comm = C.c_void_p()
+        X.call("fr_nccl_init", uid, self.world, self.rank, C.byref(self.comm))
+        self.dtype = X.F32 if dtype == "float32" else X.F64
+
+    def __call__(self, sends, recvs, send_bufs, recv_bufs, group=None):
+        sp, sb, sc, rp, rb, rc = [], [], [], [], [], []
+        for dest, k, _ in sends:
+            for t in send_bufs[k]:
+                sp.append(dest), sb.append(t.data_ptr()), sc.append(t.numel())
+        for src, gi, _ in recvs:
+            for t in recv_bufs[gi]:
+                rp.append(src), rb.append(t.data_ptr()), rc.append(t.numel())
+        arr = lambda ty, v: (ty * max(len(v), 1))(*v)  # noqa: E731
+        X.call("fr_exchange", self.comm, len(sp), arr(C.c_int, sp), arr(C.c_void_p, sb), arr(C.c_longlong, sc),
+               len(rp), arr(C.c_int, rp), arr(C.c_void_p, rb), arr(C.c_longlong, rc), self.dtype, X.stream_ptr())
+        return []  # enqueued on the current stream: nothing to wait for
+
+    def close(self):
+        if self.comm:
+            X.call("fr_nccl_destroy", self.comm)
+            self.comm = C.c_void_p()
+
+
 class DistributedTrainer:
     """This process's rank of a torch.distributed group (NCCL over NVLink).
 
@@ -321,8 +360,12 @@ class DistributedTrainer:
     stream order (it also brings up the NCCL connections, which may
     synchronise the device)."""
 
-    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=None):
+    def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=None,
+                 transport="torch"):
         import torch.distributed as dist
+
+        if transport not in ("torch", "fr_nccl"):
+            raise ValueError(f"unknown transport {transport!r} (use 'torch' or 'fr_nccl')")
 
         self.plan = plan
         self.rank = dist.get_rank() if rank is None else rank
@@ -350,6 +393,9 @@ class DistributedTrainer:
                           + ((w.objective.target_du_slice(gi),) if w.send_derivatives else ())
                           for _, gi, _ in self.recvs}
         self._connected = False
+        # exchange rounds: torch.distributed batched P2P, or the library's own
+        # NCCL transport (fr_exchange)
+        self._post = FrNcclTransport(dtype) if transport == "fr_nccl" else None
         if self.overlap:
             self.comm = torch.cuda.Stream()
             self.gate_word = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -377,7 +423,7 @@ class DistributedTrainer:
             w.objective.mark_targets_set()
             self.comm.wait_event(ready)
             with torch.cuda.stream(self.comm):
-                for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                for wk in (self._post or post_exchange)(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                     wk.wait()  # transport stream waits for the transfers
                 X.call("fr_signal", C.c_void_p(self.gate_word.data_ptr()), 1, 0, X.stream_ptr(self.comm))
             # the next round reuses the send buffers and targets
@@ -387,7 +433,7 @@ class DistributedTrainer:
                 w.produce()
                 for k, _ in enumerate(self.sends):
                     w.pack_edge(k, *self.send_bufs[k][:2], out_du=self._du(k))
-                for wk in post_exchange(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
+                for wk in (self._post or post_exchange)(self.sends, self.recvs, self.send_bufs, self.recv_bufs):
                     wk.wait()  # orders the compute stream after the transfers (no host sync)
                 self._connected = True
                 w.objective.mark_targets_set()

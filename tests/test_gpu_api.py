@@ -76,3 +76,35 @@ def test_no_cpu_fallback_library_is_the_compute_path():
     before = X.kernel_launches()
     predict(init_params(ExpertConfig(3, 2, 16, "tanh", 3), 0), np.zeros((10, 3)))
     assert X.kernel_launches() > before
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_nccl_transport_self_exchange(dtype):
+    """fr_nccl_init / fr_exchange on a one-rank communicator: a grouped round
+    of sends to and receives from this rank moves every buffer (the C-ABI
+    transport of SURVEY 8b; multi-rank rounds need more GPUs than this box)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2602_15883_b200 import _lib as X
+
+    uid = C.create_string_buffer(128)
+    X.call("fr_nccl_get_unique_id", uid)
+    comm = C.c_void_p()
+    X.call("fr_nccl_init", uid, 1, 0, C.byref(comm))
+    T = torch.float32 if dtype == "float32" else torch.float64
+    src = [torch.arange(n, dtype=T, device="cuda") * (k + 1) for k, n in enumerate((1000, 3000, 7))]
+    dst = [torch.zeros_like(t) for t in src]
+    ptrs = lambda ts: (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
+    cnts = (C.c_longlong * 3)(*[t.numel() for t in src])
+    peers = (C.c_int * 3)(0, 0, 0)
+    X.call("fr_exchange", comm, 3, peers, ptrs(src), cnts, 3, peers, ptrs(dst), cnts,
+           X.F32 if dtype == "float32" else X.F64, X.stream_ptr())
+    torch.cuda.synchronize()
+    for a, b in zip(src, dst):
+        assert torch.equal(a, b)
+    bad = (C.c_int * 1)(1)
+    with pytest.raises(X.FlowrecError, match="peer 1"):
+        X.call("fr_exchange", comm, 1, bad, ptrs(src[:1]), cnts, 0, None, None, None, X.F32, X.stream_ptr())
+    X.call("fr_nccl_destroy", comm)
