@@ -49,7 +49,9 @@ def needs_build():
 
 def _compile(src, defines=(), out_dir=OUT_DIR):
     obj = os.path.join(out_dir, os.path.splitext(src)[0] + ".o")
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = os.environ.get("FR_NVCC_EXTRA", "").split()  # side-build experiments only
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c", os.path.join(CSRC, src),
+           "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
