@@ -311,6 +311,10 @@ __device__ __forceinline__ void store_block_f2(float* __restrict__ buf, int rg, 
   }
 }
 
+template <typename T, int W, int RPT, int RS4>
+__device__ __forceinline__ void gemm_rows_scalar(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
+                                                 T (&acc)[RPT][8]);
+
 // acc[r][j] = sum_k A(rg*RPT + r, k) * B[k][unit_of(g, j)]
 template <typename T, int W, int RPT, int RS4>
 __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
@@ -327,8 +331,15 @@ __device__ __forceinline__ void gemm_rows(const T* __restrict__ A, const T* __re
         acc[r][2 * q] = T(x);
         acc[r][2 * q + 1] = T(y);
       }
-    return;
+  } else {
+    gemm_rows_scalar<T, W, RPT, RS4>(A, B, rg, g, acc);
   }
+}
+
+// FP64 (parity build): plain FMA chain, k ascending
+template <typename T, int W, int RPT, int RS4>
+__device__ __forceinline__ void gemm_rows_scalar(const T* __restrict__ A, const T* __restrict__ B, int rg, int g,
+                                                 T (&acc)[RPT][8]) {
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
 #pragma unroll
