@@ -1,10 +1,30 @@
 // TF32 tensor-core wide-expert training kernels (PDE and MSE heads), FP32 I/O.
 #include "jetmlp_dispatch.cuh"
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "tcwide_kernel.cuh"
 
 namespace fr {
+
+// FR_TC_FWD=tile selects the one-tile-per-CTA forward (A/B measurements)
+static bool tc_persistent_fwd() {
+  static const bool v = [] {
+    const char* e = getenv("FR_TC_FWD");
+    return !(e && std::string(e) == "tile");
+  }();
+  return v;
+}
+static int tc_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
 
 template <int ACT, int MODE, int REG>
 int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
@@ -21,13 +41,22 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(tcw_fwd_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
+    cudaFuncSetAttribute(tcw_fwdp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(float) * TCP_NS * C::stage_floats(256)));
     cudaFuncSetAttribute(tcw_dx_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
     cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tcw_head_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::head_smem(512)));
     attrs = true;
   }
   const dim3 gt(a.ntiles, a.WP / NB);
-  for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, TC_FWD_NT, C::gemm_smem(NB), st>>>(a, l);
+  if (tc_persistent_fwd()) {
+    const long long items = (long long)a.ntiles * (a.WP / NB);
+    const int grid = int(std::min<long long>(items, tc_num_sms()));
+    const size_t smem = sizeof(float) * TCP_NS * C::stage_floats(NB);
+    for (int l = 1; l < a.L; ++l) tcw_fwdp_kernel<ACT, MODE, REG><<<grid, TCP_FWD_NT, smem, st>>>(a, l);
+  } else {
+    for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, TC_FWD_NT, C::gemm_smem(NB), st>>>(a, l);
+  }
   tcw_head_kernel<ACT, MODE, REG><<<a.ntiles, C::NT, C::head_smem(a.WP), st>>>(a);
   for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, TC_DX_NT, C::gemm_smem(NB), st>>>(a, l);
   // dW: all ceil(WP/128) k-blocks of an N block accumulate in TMEM (<= 512

@@ -353,6 +353,164 @@ __global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
 }
 
 // ---------------------------------------------------------------------------
+// persistent forward, hidden layer l >= 1 (same math as tcw_fwd_kernel).
+// One CTA per SM walks the (tile, N block) items grid-strided, so the HBM
+// stream never drains at tile boundaries: an 8-stage ring, and two TMEM
+// accumulators (2 x 256 columns) so the MMAs of item i+1 run while dedicated
+// epilogue warps drain item i to HBM.
+//   warps 0..3   jet activation in place            warp 4  bulk-copy loader
+//   warp 5       MMA issuer                          warps 6..9  S_{l-1} row-quad-major copy
+//   warps 10..13 epilogue TMEM -> Z_l (+ b on value rows), frees the accumulator
+// Stage s and accumulator b phases follow the CTA-local chunk / item counters.
+// ---------------------------------------------------------------------------
+constexpr int TCP_NS = 8;
+constexpr int TCP_FWD_NT = 576;
+template <int ACT, int MODE, int REG>
+__global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l) {
+  using C = TcCfg<ACT, MODE, REG>;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  float* ring = reinterpret_cast<float*>(tc_smem);
+  __shared__ __align__(8) uint64_t full[TCP_NS], actd[TCP_NS], mmad[TCP_NS], std_[TCP_NS], accf[2], acce[2];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NB = a.nb, nnb = a.WP / NB;
+  const long long nitems = (long long)a.ntiles * nnb;
+  const float* kp = static_cast<const float*>(a.kp);
+  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
+  if (tid == 0) {
+    for (int i = 0; i < TCP_NS; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&actd[i], 4);
+      tc::mbar_init(&std_[i], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&accf[b], 1);
+      tc::mbar_init(&acce[b], 4);
+    }
+  }
+  const uint32_t tmem = tc_setup<512>(&tslot, mmad, TCP_NS);
+  const int nch = a.WP / TC_KC;
+  const bool virt = (l == 1);
+  const size_t SF = C::stage_floats(NB);
+  auto arrive = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+  };
+  if (warp == 8) {
+    if (lane == 0) {
+      long long g = 0;
+      for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const long long tile = w / nnb;
+        const int nb = int(w % nnb);
+        const float* zsrc = static_cast<const float*>(a.act) + (virt ? 0 : tc_off(a, l - 1, tile, 0));
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = int(g % TCP_NS);
+          if (g >= TCP_NS) {
+            const uint32_t ph = uint32_t((g - TCP_NS) / TCP_NS) & 1;
+            tc::mbar_wait(&mmad[s], ph);
+            tc::mbar_wait(&std_[s], ph);
+          }
+          float* st = ring + s * SF;
+          tc::mbar_expect_tx(&full[s], NB * 64 + (virt ? 0 : 8192));
+          tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
+          if (!virt) tc::bulk_g2s(st, zsrc + size_t(c) * 2048, 8192, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, NB);
+      long long g = 0, it = 0;
+      for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const int b = int(it & 1);
+        if (it >= 2) {
+          tc::mbar_wait(&acce[b], uint32_t((it - 2) >> 1) & 1);
+          tc::fence_after();
+        }
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = int(g % TCP_NS);
+          float* A = ring + s * SF;
+          tc::mbar_wait(&actd[s], uint32_t(g / TCP_NS) & 1);
+          tc::fence_after();
+          tc_mma16(tmem + b * 256, A, 128, A + 2048, NB, idesc, c == 0);
+          tc::mma_commit(&mmad[s]);
+        }
+        tc::mma_commit(&accf[b]);
+      }
+    }
+  } else if (warp >= 10 && warp < 14) {
+    const int t = tid - 320;
+    long long g = 0;
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
+      const long long tile = w / nnb;
+      const bool st0 = (w % nnb) == 0;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int s = int(g % TCP_NS);
+        tc::mbar_wait(&actd[s], uint32_t(g / TCP_NS) & 1);
+        if (st0) slab_store_t<C>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
+        arrive(&std_[s]);
+      }
+    }
+  } else if (warp >= 14) {
+    const int q = warp & 3, r = q * 32 + lane;
+    const bool vrow = lane < C::VR && (lane % C::S) == 0;
+    long long it = 0;
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+      const long long tile = w / nnb;
+      const int b = int(it & 1), n0 = int(w % nnb) * NB;
+      tc::mbar_wait(&accf[b], uint32_t(it >> 1) & 1);
+      tc::fence_after();
+      float* Zo = static_cast<float*>(a.act) + tc_off(a, l, tile, n0 / 4) + r * 4;
+      const float* bl = kp + pl.off_b(l) + n0;
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + b * 256 + c0, v);
+        if (vrow)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += __ldg(bl + c0 + i);
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          __stcs(reinterpret_cast<float4*>(Zo + size_t(c0 / 4 + h) * 512),
+                 make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]));
+      }
+      tc::fence_before();
+      arrive(&acce[b]);
+    }
+  } else {
+    // two activation groups (warps 0..3, 4..7) take alternate chunks
+    const int ag = warp >> 2, t = tid & 127;
+    long long g = 0;
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
+      const long long tile = w / nnb;
+      for (int c = 0; c < nch; ++c, ++g) {
+        if (int(g & 1) != ag) continue;
+        const int s = int(g % TCP_NS);
+        float* A = ring + s * SF;
+        tc::mbar_wait(&full[s], uint32_t(g / TCP_NS) & 1);
+        for (int i = t; i < C::ITEMS; i += 128) {
+          const int pt = i % C::PPT, kq = i / C::PPT;
+          float z[C::S][4], sv[C::S][4];
+          if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, 4 * c + kq, z);
+          else slab_load<C>(z, A, pt, kq);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float zz[C::S], ss[C::S];
+            col<C>(z, j, zz);
+            tc_act1<C, ACT>(zz, ss);
+#pragma unroll
+            for (int k = 0; k < C::S; ++k) sv[k][j] = ss[k];
+          }
+          slab_store<C>(A, pt, kq, sv);
+        }
+        tc::fence_proxy_async();
+        arrive(&actd[s]);
+      }
+    }
+  }
+  tc_teardown<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
 // adjoint, hidden layer l >= 1: Zbar_{l-1} = act_bwd(Z_{l-1}, Zbar_l W_l^T)
 // grid (tiles, WP/NB), 256 threads.  Main loop: thread 0 streams Zbar_l and W_l
 // slabs through the ring and issues the MMAs.  Epilogue, 16 TMEM columns per
