@@ -8,10 +8,18 @@
 
 namespace fr {
 
-// FR_TC_FWD=tile selects the one-tile-per-CTA forward (A/B measurements)
+// FR_TC_FWD=tile / FR_TC_DX=tile select the one-tile-per-CTA forward / adjoint
+// kernels (A/B measurements)
 static bool tc_persistent_fwd() {
   static const bool v = [] {
     const char* e = getenv("FR_TC_FWD");
+    return !(e && std::string(e) == "tile");
+  }();
+  return v;
+}
+static bool tc_persistent_dx() {
+  static const bool v = [] {
+    const char* e = getenv("FR_TC_DX");
     return !(e && std::string(e) == "tile");
   }();
   return v;
@@ -44,6 +52,8 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
     cudaFuncSetAttribute(tcw_fwdp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(float) * TCP_NS * C::stage_floats(256)));
     cudaFuncSetAttribute(tcw_dx_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
+    cudaFuncSetAttribute(tcw_dxp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(tcp_dx_smem<C>(256)));
     cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tcw_head_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::head_smem(512)));
     attrs = true;
@@ -58,7 +68,13 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
     for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, TC_FWD_NT, C::gemm_smem(NB), st>>>(a, l);
   }
   tcw_head_kernel<ACT, MODE, REG><<<a.ntiles, C::NT, C::head_smem(a.WP), st>>>(a);
-  for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, TC_DX_NT, C::gemm_smem(NB), st>>>(a, l);
+  if (tc_persistent_dx()) {
+    const long long items = (long long)a.ntiles * (a.WP / NB);
+    const int grid = int(std::min<long long>(items, tc_num_sms()));
+    for (int l = a.L - 1; l >= 1; --l) tcw_dxp_kernel<ACT, MODE, REG><<<grid, TCP_DX_NT, tcp_dx_smem<C>(NB), st>>>(a, l);
+  } else {
+    for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, TC_DX_NT, C::gemm_smem(NB), st>>>(a, l);
+  }
   // dW: all ceil(WP/128) k-blocks of an N block accumulate in TMEM (<= 512
   // columns); N block = the largest multiple of 16 dividing WP that fits
   const int nkb = (a.WP + 127) / 128;

@@ -681,6 +681,223 @@ __global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
 }
 
 // ---------------------------------------------------------------------------
+// persistent adjoint, hidden layer l >= 1 (same math as tcw_dx_kernel).  One
+// CTA per SM walks the (tile, N block) items grid-strided; the MMAs of item
+// i+1 accumulate in the second TMEM buffer while the epilogue drains item i.
+//   warps 0..3  epilogue: S-bar TMEM -> shared, Z_{l-1} act-bwd in place (the
+//               Z_{l-1} slabs are prefetched two 16-unit steps ahead, across
+//               item boundaries), l == 1: dW_0 | db_0 tile partials
+//   warps 4..7  writers: Zbar_{l-1} slabs to HBM in both layouts
+//   warp 8      bulk-copy loader (Zbar_l + W_l slabs)    warp 9  MMA issuer
+// ---------------------------------------------------------------------------
+constexpr int TCP_DX_NS = 4;
+constexpr int TCP_DX_NT = 576;
+template <class C>
+__host__ __device__ constexpr int tcp_dx_epi() {  // floats of one epilogue group's buffers
+  return 4 * 2048 > 2048 + C::PPT * 16 * (C::DIN + 1) ? 4 * 2048 : 2048 + C::PPT * 16 * (C::DIN + 1);
+}
+template <class C>
+__host__ __device__ constexpr size_t tcp_dx_smem(int NB) {
+  // epilogue: stg[2] + zc[2] slabs, or (l == 1) stg[0] + the dW_0 reduction buffer
+  return sizeof(float) * (TCP_DX_NS * C::stage_floats(NB) + 2 * tcp_dx_epi<C>());
+}
+template <int ACT, int MODE, int REG>
+__global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
+  using C = TcCfg<ACT, MODE, REG>;
+  constexpr int DIN = C::DIN, D1 = DIN + 1;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  float* ring = reinterpret_cast<float*>(tc_smem);
+  __shared__ __align__(8) uint64_t full[TCP_DX_NS], empty[TCP_DX_NS], accf[2], acce[2], zfull_[2][2], rdy_[2][2], done_[2][2];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NB = a.nb, nnb = a.WP / NB, nck = NB / 16;
+  const long long nitems = (long long)a.ntiles * nnb;
+  const float* kp = static_cast<const float*>(a.kp);
+  const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
+  if (tid == 0) {
+    for (int i = 0; i < TCP_DX_NS; ++i) tc::mbar_init(&full[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 4);
+      for (int j = 0; j < 2; ++j) {
+        tc::mbar_init(&zfull_[i][j], 1);
+        tc::mbar_init(&rdy_[i][j], 4);
+        tc::mbar_init(&done_[i][j], 4);
+      }
+    }
+  }
+  const uint32_t tmem = tc_setup<512>(&tslot, empty, TCP_DX_NS);
+  const int nch = a.WP / TC_KC;
+  const size_t SF = C::stage_floats(NB);
+  const bool virt = (l == 1);
+  // epilogue group grp (items with it % 2 == grp, i.e. TMEM accumulator grp)
+  const int grp = warp >= 10 ? 1 : 0, wl = warp - 10 * grp;
+  float* stg = ring + TCP_DX_NS * SF + grp * tcp_dx_epi<C>();  // [2][4][128][4]  S-bar / Zbar columns
+  float* zc = stg + 2 * 2048;          // [2][4][128][4]  Z_{l-1} slabs
+  float* red = stg + 2048;             // l == 1: [PPT][4 kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
+  uint64_t* zfull = zfull_[grp];
+  uint64_t* rdy = rdy_[grp];
+  uint64_t* done = done_[grp];
+  auto arrive = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+  };
+  auto sync_e = [grp] { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+  if (warp == 8) {
+    if (lane == 0) {
+      long long g = 0;
+      for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const long long tile = w / nnb;
+        const int nb = int(w % nnb);
+        const float* zb = static_cast<const float*>(a.adj) + tc_off(a, l, tile, 0);
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = int(g % TCP_DX_NS);
+          if (g >= TCP_DX_NS) tc::mbar_wait(&empty[s], uint32_t((g - TCP_DX_NS) / TCP_DX_NS) & 1);
+          float* st = ring + s * SF;
+          tc::mbar_expect_tx(&full[s], NB * 64 + 8192);
+          tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_d, l, nb, c), NB * 64, &full[s]);
+          tc::bulk_g2s(st, zb + size_t(c) * 2048, 8192, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, NB);
+      long long g = 0, it = 0;
+      for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const int b = int(it & 1);
+        if (it >= 2) {
+          tc::mbar_wait(&acce[b], uint32_t((it - 2) >> 1) & 1);
+          tc::fence_after();
+        }
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = int(g % TCP_DX_NS);
+          float* st = ring + s * SF;
+          tc::mbar_wait(&full[s], uint32_t(g / TCP_DX_NS) & 1);
+          tc::fence_after();
+          tc_mma16(tmem + b * 256, st, 128, st + 2048, NB, idesc, c == 0);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&accf[b]);
+      }
+    }
+  } else if (wl < 4) {
+    const int r = (warp & 3) * 32 + lane, et = r;
+    const float* pts = static_cast<const float*>(a.pts);
+    // Z_{l-1} slab of step j of item w (16 units)
+    auto zslab = [&](long long w, int j) {
+      return static_cast<const float*>(a.act) + tc_off(a, l - 1, w / nnb, int(w % nnb) * NB / 4) + size_t(j) * 2048;
+    };
+    auto prefetch = [&](long long w, int j, int b) {  // step j of item w into zc[b] (j may run into the next item)
+      if (j >= nck) {
+        w += 2 * gridDim.x;
+        j -= nck;
+      }
+      if (w >= nitems) return;
+      tc::mbar_expect_tx(&zfull[b], 8192);
+      tc::bulk_g2s(zc + b * 2048, zslab(w, j), 8192, &zfull[b]);
+    };
+    const long long w0 = blockIdx.x + (long long)grp * gridDim.x;
+    if (!virt && et == 0 && w0 < nitems)
+      for (int j = 0; j < 2; ++j) prefetch(w0, j, j);
+    long long k = 0, jg = 0;
+    for (long long w = w0; w < nitems; w += 2 * gridDim.x, ++k) {
+      const long long tile = w / nnb;
+      const int ab = grp, n0 = int(w % nnb) * NB;
+      tc::mbar_wait(&accf[ab], uint32_t(k) & 1);
+      tc::fence_after();
+      for (int j = 0; j < nck; ++j, ++jg) {
+        const int b = virt ? 0 : int(jg & 1);
+        float* sg = stg + b * 2048;
+        if (!virt && jg >= 2) tc::mbar_wait(&done[b], uint32_t((jg - 2) >> 1) & 1);
+        {
+          float v[16];
+          tc::tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + ab * 256 + 16 * j, v);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(sg + q * 512 + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        if (j == nck - 1) {
+          tc::fence_before();
+          arrive(&acce[ab]);
+        }
+        sync_e();
+        if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
+        const float* zs = zc + b * 2048;
+        for (int i = et; i < C::ITEMS; i += 128) {
+          const int pt = i % C::PPT, kq = i / C::PPT;
+          const int q = n0 / 4 + 4 * j + kq;
+          float z[C::S][4], sb[C::S][4];
+          if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
+          else slab_load<C>(z, zs, pt, kq);
+          slab_load<C>(sb, sg, pt, kq);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            float zz[C::S], bb[C::S], sa[C::S];
+            col<C>(z, jj, zz);
+            col<C>(sb, jj, bb);
+            tc_act_bwd1<C, ACT>(zz, bb, sa);
+#pragma unroll
+            for (int k = 0; k < C::S; ++k) sb[k][jj] = bb[k];
+          }
+          if (!virt) {
+            slab_store<C>(sg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
+          } else {
+            const long long p = tile * C::PPT + pt;
+            const bool live = p < a.n;
+            float x[DIN];
+#pragma unroll
+            for (int ii = 0; ii < DIN; ++ii) x[ii] = live ? pts[p * DIN + ii] : 0.f;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+              const float zv = live ? sb[0][jj] : 0.f;
+#pragma unroll
+              for (int ii = 0; ii < DIN; ++ii) {
+                float t = x[ii] * zv;
+                if constexpr (C::JET) t += live ? sb[1 + ii][jj] : 0.f;
+                rd[ii] = t;
+              }
+              rd[DIN] = zv;
+            }
+          }
+        }
+        sync_e();
+        if (!virt) {
+          if (et == 0) prefetch(w, j + 2, b);
+          arrive(&rdy[b]);
+        } else {
+          for (int e = et; e < 16 * D1; e += 128) {
+            const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
+            float acc = 0.f;
+            for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + jj) * D1 + ii];
+            const int u = n0 + 16 * j + 4 * kq + jj;
+            a.p0[size_t(tile) * (D1 * a.WP) + size_t(ii) * a.WP + u] = acc;
+          }
+          sync_e();
+        }
+      }
+    }
+  } else if (!virt) {
+    const int t = (wl - 4) * 32 + lane;
+    long long jg = 0;
+    for (long long w = blockIdx.x + (long long)grp * gridDim.x; w < nitems; w += 2 * gridDim.x) {
+      const long long tile = w / nnb;
+      const int n0 = int(w % nnb) * NB;
+      for (int j = 0; j < nck; ++j, ++jg) {
+        const int b = int(jg & 1);
+        tc::mbar_wait(&rdy[b], uint32_t(jg >> 1) & 1);
+        const float* sg = stg + b * 2048;
+        slab_copy_out(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
+        slab_store_t<C>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+        arrive(&done[b]);
+      }
+    }
+  }
+  tc_teardown<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
 // dW_l = sum_rows S_{l-1}^T Zbar_l (+ db_l = sum of value rows of Zbar_l).
 // Both operands arrive row-quad major (written by the forward / adjoint
 // kernels), i.e. already K-major for K = rows, so this is a pure stream:
