@@ -424,6 +424,15 @@ def run_ours(args):
             "host_launches_timed": launches_host,
             "host_enqueue_ms_per_step": host_s / args.steps * 1e3,
         }
+        if hbm and hbm["peak_gbs"]:
+            # the layer-wise TF32 launches are HBM-bound by construction: the
+            # roofline is the activation-slab bytes against the measured copy bandwidth, the
+            # tensor-pipe figure rides along
+            rf = line["roofline"]
+            tensor = {k: rf.pop(k) for k in ("achieved", "peak", "unit", "frac", "peak_source")}
+            rf.update({"bound": "hbm", "achieved": hbm["achieved_gbs"], "peak": hbm["peak_gbs"], "unit": "GB/s",
+                       "frac": hbm["frac"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
+                       "bytes_per_launch": hbm["bytes_per_launch"], "tensor": tensor})
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_seconds)
         print(json.dumps(line), flush=True)
