@@ -88,6 +88,46 @@ __device__ __forceinline__ void tc_z0(const WArgs& a, const float* __restrict__ 
   }
 }
 
+// layer-0 pre-activation jet of point p (global index), unit u
+template <class C>
+__device__ __forceinline__ void tc_z0u(const WArgs& a, const float* __restrict__ kp, const ParamLayout& pl,
+                                       long long p, int u, float (&z)[C::S]) {
+  const float* pts = static_cast<const float*>(a.pts);
+  float zv = 0.f;
+#pragma unroll
+  for (int i = 0; i < C::DIN; ++i) zv = fmaf(p < a.n ? pts[p * C::DIN + i] : 0.f, kp[pl.off_w(0) + i * a.WP + u], zv);
+  z[0] = zv + kp[pl.off_b(0) + u];
+  if constexpr (C::JET) {
+#pragma unroll
+    for (int i = 0; i < C::NG; ++i) z[1 + i] = kp[pl.off_w(0) + i * a.WP + u];
+#pragma unroll
+    for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i] = 0.f;
+  }
+}
+
+// per-unit item split of the persistent kernels' activation steps: when the
+// (point, unit quad) items of a 16-unit chunk fill at most half of the 128
+// threads (3D jets: 64 items), each thread takes single (point, quad, unit)
+// items instead (measured: E -12% epoch time; for the 2D jets' 80 items the
+// 3-round split with scalar shared loads was a wash)
+template <class C>
+struct TcUnit {
+  static constexpr bool ON = 2 * C::ITEMS <= 128;
+  static constexpr int N = ON ? C::ITEMS * 4 : C::ITEMS;
+};
+template <class C>
+__device__ __forceinline__ void slab_load1(float (&v)[C::S], const float* slab, int pt, int kq, int j) {
+  const float* b = slab + kq * 512 + C::row0(pt) * 4 + j;
+#pragma unroll
+  for (int s = 0; s < C::S; ++s) v[s] = b[4 * s];
+}
+template <class C>
+__device__ __forceinline__ void slab_store1(float* slab, int pt, int kq, int j, const float (&v)[C::S]) {
+  float* b = slab + kq * 512 + C::row0(pt) * 4 + j;
+#pragma unroll
+  for (int s = 0; s < C::S; ++s) b[4 * s] = v[s];
+}
+
 // jet activation of one point / unit: s = sigma applied to the stacked jet
 template <class C, int ACT>
 __device__ __forceinline__ void tc_act1(const float (&z)[C::S], float (&s)[C::S]) {
@@ -487,6 +527,16 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
         const int s = int(g % TCP_NS);
         float* A = ring + s * SF;
         tc::mbar_wait(&full[s], uint32_t(g / TCP_NS) & 1);
+        if constexpr (TcUnit<C>::ON) {
+          for (int i = t; i < TcUnit<C>::N; i += 128) {
+            const int j = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
+            float z[C::S], sv[C::S];
+            if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, 16 * c + 4 * kq + j, z);
+            else slab_load1<C>(z, A, pt, kq, j);
+            tc_act1<C, ACT>(z, sv);
+            slab_store1<C>(A, pt, kq, j, sv);
+          }
+        } else
         for (int i = t; i < C::ITEMS; i += 128) {
           const int pt = i % C::PPT, kq = i / C::PPT;
           float z[C::S][4], sv[C::S][4];
@@ -824,6 +874,31 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         sync_e();
         if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
         const float* zs = zc + b * 2048;
+        if constexpr (TcUnit<C>::ON) {
+          for (int i = et; i < TcUnit<C>::N; i += 128) {
+            const int jj = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
+            float z[C::S], sb[C::S], sa[C::S];
+            if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 16 * j + 4 * kq + jj, z);
+            else slab_load1<C>(z, zs, pt, kq, jj);
+            slab_load1<C>(sb, sg, pt, kq, jj);
+            tc_act_bwd1<C, ACT>(z, sb, sa);
+            if (!virt) {
+              slab_store1<C>(sg, pt, kq, jj, sb);  // Zbar_{l-1}, in place of S-bar
+            } else {
+              const long long p = tile * C::PPT + pt;
+              const bool live = p < a.n;
+              float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+              const float zv = live ? sb[0] : 0.f;
+#pragma unroll
+              for (int ii = 0; ii < DIN; ++ii) {
+                float t = (live ? pts[p * DIN + ii] : 0.f) * zv;
+                if constexpr (C::JET) t += live ? sb[1 + ii] : 0.f;
+                rd[ii] = t;
+              }
+              rd[DIN] = zv;
+            }
+          }
+        } else
         for (int i = et; i < C::ITEMS; i += 128) {
           const int pt = i % C::PPT, kq = i / C::PPT;
           const int q = n0 / 4 + 4 * j + kq;
