@@ -39,3 +39,49 @@ def test_tc_gemm_tf32(N, K):
     # truncation vs round-to-nearest of the TF32 conversion: bound by 2^-10 per product
     err = np.abs(C - ref) / scale
     assert err.max() < 2.0 ** -10, (err.max(), np.abs(C - full).max())
+
+
+_PERSIST_SCRIPT = r"""
+import hashlib, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["FR_ROOT"])
+from paper_2602_15883_b200 import engine
+from paper_2602_15883_b200.network import ExpertConfig, init_params
+out = []
+for kind, d, w, L, act in [("unsteady2d", 3, 150, 4, "sin"), ("unsteady3d", 4, 200, 3, "sin"),
+                           ("steady2d", 2, 128, 3, "tanh")]:
+    cfg = ExpertConfig(d, L, w, act, d if kind != "steady2d" else 3)
+    p = init_params(cfg, 1).flat
+    rng = np.random.default_rng(2)
+    n = 5003  # a ragged last tile
+    pts = rng.uniform(-2.0, 2.0, (n, d))
+    plan = engine.get_plan(cfg, kind, 100.0, "float32", math="tf32")
+    sq, g = engine.pde_loss_grad(plan, p, pts, 1.0 / n)
+    nv = cfg.arch[-1] - 1
+    su, sp, gm = engine.mse_loss_grad(plan, p, pts[:777], rng.standard_normal((777, nv)), rng.standard_normal(777),
+                                     np.ones(nv), 0.3, 0.7)
+    out.append(hashlib.sha256(np.float64([sq, su, sp]).tobytes() + g.tobytes() + gm.tobytes()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def test_tc_persistent_kernels_bit_identical_to_tile_kernels():
+    """The persistent TF32 forward / adjoint kernels (default) compute exactly
+    what the one-tile-per-CTA kernels do (FR_TC_FWD=tile / FR_TC_DX=tile):
+    same MMA K order, same per-point epilogue arithmetic, so losses and both
+    PDE and MSE gradients are bit-identical, incl. a ragged last tile, the 3D
+    per-unit activation split and the steady regime."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("persistent", "tile"):
+        env = dict(os.environ, FR_ROOT=root, FR_TC_FWD=mode, FR_TC_DX=mode)
+        r = subprocess.run([sys.executable, "-c", _PERSIST_SCRIPT], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = r.stdout.split()
+    assert len(res["persistent"]) == 3
+    assert res["persistent"] == res["tile"]
