@@ -108,11 +108,12 @@ __device__ __forceinline__ void tc_z0u(const WArgs& a, const float* __restrict__
 // per-unit item split of the persistent kernels' activation steps: when the
 // (point, unit quad) items of a 16-unit chunk fill at most half of the 128
 // threads (3D jets: 64 items), each thread takes single (point, quad, unit)
-// items instead (measured: E -12% epoch time; for the 2D jets' 80 items the
-// 3-round split with scalar shared loads was a wash)
-template <class C>
+// items instead (measured: E -12% epoch time).  For the 2D jets' 80 items the
+// 3-round split with scalar shared loads pays only in the sin adjoint (D150
+// dx -2.8%; forward +2%, tanh adjoint +7%)
+template <class C, bool ADJ = false, int ACT = ACT_TANH>
 struct TcUnit {
-  static constexpr bool ON = 2 * C::ITEMS <= 128;
+  static constexpr bool ON = 2 * C::ITEMS <= 128 || (ADJ && ACT == ACT_SIN && (C::ITEMS % 128) != 0);
   static constexpr int N = ON ? C::ITEMS * 4 : C::ITEMS;
 };
 template <class C>
@@ -874,8 +875,8 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         sync_e();
         if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
         const float* zs = zc + b * 2048;
-        if constexpr (TcUnit<C>::ON) {
-          for (int i = et; i < TcUnit<C>::N; i += 128) {
+        if constexpr (TcUnit<C, true, ACT>::ON) {
+          for (int i = et; i < TcUnit<C, true, ACT>::N; i += 128) {
             const int jj = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
             float z[C::S], sb[C::S], sa[C::S];
             if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 16 * j + 4 * kq + jj, z);
