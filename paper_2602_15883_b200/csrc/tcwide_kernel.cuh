@@ -1098,6 +1098,10 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   using C = TcCfg<ACT, MODE, REG>;
   constexpr int NT = C::NT, PPT = C::PPT, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
   constexpr int NG = C::NG, LAP0 = C::LAP0, SN = S * NOUT;
+  // 3D jets: 64 (point, unit quad) items per chunk -> per-unit items (TcUnit)
+  constexpr bool HU = TcUnit<C>::ON;
+  constexpr int TPPH = HU ? NT / PPT : C::TPP;  // threads holding partial sums of one point
+  static_assert(!HU || (NT % (4 * PPT) == 0 && 4 * C::ITEMS % NT == 0), "per-unit head split");
   extern __shared__ __align__(128) unsigned char tc_smem[];
   double* lred = reinterpret_cast<double*>(tc_smem);      // [2][NT]
   float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][2048]
@@ -1136,6 +1140,20 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   for (int c = 0; c < nch; ++c) {
     const int s = c % TC_NS;
     tc::mbar_wait(&full[s], (c / TC_NS) & 1);
+    if constexpr (HU) {
+      // per-unit items: thread tid always holds point (tid >> 2) % PPT
+      for (int i = tid; i < 4 * C::ITEMS; i += NT) {
+        const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
+        float zz[S], ss[S];
+        slab_load1<C>(zz, ring + s * 2048, pt, kq, j);
+        tc_act1<C, ACT>(zz, ss);
+        const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
+#pragma unroll
+        for (int st = 0; st < S; ++st)
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o) y[st][o] = fmaf(ss[st], w[o], y[st][o]);
+      }
+    } else
     for (int i = tid; i < C::ITEMS; i += NT) {
       const int pt = i % PPT, kq = i / PPT;
       float z[S][4];
@@ -1168,7 +1186,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     float* yb = Ybs + pt * SN;
     for (int i = 0; i < SN; ++i) {
       float v = 0.f;
-      for (int h = 0; h < C::TPP; ++h) v += Yp[(pt + PPT * h) * SN + i];
+      for (int h = 0; h < TPPH; ++h) v += Yp[(HU ? 4 * (pt + PPT * (h >> 2)) + (h & 3) : pt + PPT * h) * SN + i];
       yv[i] = (i < NOUT) ? v + kp[pl.off_b(L) + i] : v;
       yb[i] = 0.f;
     }
@@ -1258,6 +1276,32 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     const int g = nch + c, s = g % TC_NS;
     float* slab = ring + s * 2048;
     tc::mbar_wait(&full[s], (g / TC_NS) & 1);
+    if constexpr (HU) {
+      for (int i = tid; i < 4 * C::ITEMS; i += NT) {
+        const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
+        const float* yb = Ybs + pt * SN;
+        const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
+        float zz[S], bb[S], sa[S];
+        slab_load1<C>(zz, slab, pt, kq, j);
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+          float v = 0.f;
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o) v = fmaf(yb[st * NOUT + o], w[o], v);
+          bb[st] = v;
+        }
+        tc_act_bwd1<C, ACT>(zz, bb, sa);
+        float* rd = red + ((pt * 4 + kq) * 4 + j) * NOUT;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+          float v = 0.f;
+#pragma unroll
+          for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
+          rd[o] = v;
+        }
+        slab_store1<C>(slab, pt, kq, j, bb);  // Zbar_{L-1} in place of Z_{L-1}
+      }
+    } else
     for (int i = tid; i < C::ITEMS; i += NT) {
       const int pt = i % PPT, kq = i / PPT;
       const int q = 4 * c + kq;
