@@ -11,8 +11,9 @@ GPU, NCCL point-to-point ghost exchange).  value = N_pde * K / (max over ranks
 of the device time of K epochs).
 
 `--impl reference` times the reference's own CPU implementation (flowrec,
-installed under baseline/_ref) on this host's cores on a bounded sample of the
-same workload, on rank 0 only.
+installed under baseline/_ref) on this host's cores on the SAME, unsampled
+workload (full 500k-point epochs), on rank 0 only, plus the reference's own
+P=1/2/4/8 strong-scaling harness (process backend, one core per rank).
 """
 
 import argparse
@@ -616,33 +617,158 @@ def cpu_baseline(args, budget_s=15.0, n_sample=25_000):
     return _baseline_record(args, t_epochs, n_sample, n_obs, kind)
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _ref_problem(cfgd, n_procs, n_pde):
+    """The benchmark problem built with the REFERENCE's own API (flowrec:
+    benchmarks, partition, build_all_rank_datasets, build_plan), the same
+    inputs as paper_2602_15883_b200.config (bit-exact, tests/test_host.py)."""
+    from flowrec import benchmarks as B
+    from flowrec.config import decomposition_for_procs
+    from flowrec.decomposition import (Budget, GlobalDomain, ReferenceTable, build_all_rank_datasets, partition,
+                                       snapshot_observations)
+    from flowrec.network import ExpertConfig
+    from flowrec.physics import LossWeights
+
+    arch = cfgd["arch"]
+    if cfgd["kind"] == "2d":
+        sol = B.TaylorGreen2D(re=100.0, spatial_box=((-7.5, 17.5), (-8.0, 8.0)), time_interval=(0.0, 7.35))
+        nx, snaps, per_snap, n_gh, deltas = 33, 50, 200, 1000, (2.0, 1.0)
+        weights = LossWeights(10.0, 5.0, 1.0, 1.0, 1.0)
+    else:
+        sol = B.Beltrami3D(a=1.0, d=1.0, re=300.0, spatial_box=((-5.0, 20.0), (-5.0, 5.0), (0.0, 10.0)),
+                           time_interval=(0.0, 11.85))
+        nx, snaps, per_snap, n_gh, deltas = 17, 80, 1250, 5000, (2.0, 2.0)
+        weights = LossWeights(10.0, 10.0, 1.0, 1.0, 1.0, velocity=(1.0, 5.0, 100.0))
+    domain = GlobalDomain.from_solution(sol)
+    pts = B.grid_points(sol, nx, snaps)
+    vel, p = sol.velocity_pressure(pts)
+    table = ReferenceTable(regime=sol.regime, points=pts, velocity=vel, pressure=p)
+    obs = snapshot_observations(table, per_snap, seed=0)
+    counts, m = decomposition_for_procs(sol.regime, n_procs)
+    subs = partition(domain, counts, m, delta_space=deltas[0], delta_time=deltas[1])
+    ds = build_all_rank_datasets(subs, Budget(n_obs=obs.n, n_pde=n_pde, n_ghost_per_interface=n_gh), obs, 0)
+    cfg = ExpertConfig.for_regime(sol.regime, arch["hidden_layers"], arch["width"], arch["activation"])
+    anchor = tuple(lo + 0.25 * (hi - lo) for lo, hi in domain.spatial_box)
+    return subs, ds, cfg, weights, anchor, (counts, m)
+
+
+def _ref_train_epoch_time(cfgd, n_procs, n_pde, epochs):
+    """The reference's own strong-scaling harness for one P: train(plan,
+    backend="serial" at P=1 / "process" at P>1) -- one core and one BLAS
+    thread per rank (driver.py:129,186) -- and TrainResult.median_epoch_time()
+    (driver.py:65-68)."""
+    from flowrec.runtime import TrainConfig, build_plan, train
+
+    subs, ds, cfg, weights, anchor, dec = _ref_problem(cfgd, n_procs, n_pde)
+    tc = TrainConfig(epochs=epochs, batch_size=25_000, learning_rate=1e-3, weights=weights, anchor=anchor,
+                     lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0)
+    plan = build_plan(subs, ds, cfg, tc)
+    t0 = time.perf_counter()
+    res = train(plan, backend="serial" if n_procs == 1 else "process", exchange_timeout=600.0)
+    return res.median_epoch_time(), time.perf_counter() - t0, dec
+
+
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation, UNSAMPLED, on
+    this host.  N=1: every timed step is one full P=1 epoch of the config
+    (LocalObjective.epoch over all N_pde collocation points + adam_step,
+    objective.py:164-199, optim.py:31-49) with all host threads for BLAS; then
+    the reference's strong-scaling harness at P=1/2/4/8 (one core per rank) for
+    the CPU scaling column.  N>1 (torchrun): rank 0 times the reference's
+    process backend at P=N (W+K epochs, median epoch time of the last K)."""
     from threadpoolctl import threadpool_limits
 
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    with threadpool_limits(limits=os.cpu_count()):
-        step, n_sample, n_obs, kind = _reference_epoch(args)
-        for _ in range(args.warmup):
-            step()
-        t_epochs = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            step()
-            t_epochs.append(time.perf_counter() - t0)
-    vals = [_baseline_record(args, t_epochs, n_sample, n_obs, kind)]
-    v = float(np.median([x["value"] for x in vals]))
-    cb = dict(vals[-1])
-    cb["value"] = v
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": args.n_pde / v * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-            "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)",
-            "config": {"workload": f"cylinder-wake strong-scaling config {args.config}, P=1 epoch sample of "
-                                   f"N_pde={args.n_pde}, reference CPU implementation", "config_id": args.config},
-            "cpu_baseline": cb,
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    kind = _reference_module()
+    cfgd = CONFIGS[args.config]
+    cores = os.cpu_count()
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "impl": "reference",
+            "data": "synthetic (Taylor-Green stand-in on the cylinder-wake box, reference generator)"}
+    if kind != "reference":
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref (flowrec) is not installed"}), flush=True)
+        return
+    if world == 1:
+        from flowrec.network import init_params
+        from flowrec.runtime import AdamState, LocalObjective, adam_step
+
+        subs, ds, cfg, weights, _, dec = _ref_problem(cfgd, 1, args.n_pde)
+        d = ds[0]
+        with threadpool_limits(limits=cores):
+            obj = LocalObjective(cfg, subs[0].domain.regime, d, weights, 25_000)
+            params = init_params(cfg, 0)
+            st = AdamState.zeros(cfg.n_params)
+            rng = np.random.default_rng(0)
+
+            def step():
+                _, g, _ = obj.epoch(params, rng)
+                adam_step(params.flat, g, st, 1e-3)
+
+            for _ in range(args.warmup):
+                step()
+            t_epochs = []
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                step()
+                t_epochs.append(time.perf_counter() - t0)
+        t = float(np.median(t_epochs))
+        v = args.n_pde / t
+        scaling = None
+        if not args.no_cpu_scaling:
+            scaling = {"harness": "flowrec train(plan, backend='serial' P=1 | 'process' P>1), one core + one BLAS "
+                                  "thread per rank; TrainResult.median_epoch_time()",
+                       "epochs_per_P": args.cpu_scaling_epochs, "P": {}}
+            for P in (1, 2, 4, 8):
+                if P > cores:
+                    continue
+                te, wall, dec_p = _ref_train_epoch_time(cfgd, P, args.n_pde, args.cpu_scaling_epochs)
+                scaling["P"][str(P)] = {"median_epoch_s": te, "colloc_pts_per_s": args.n_pde / te,
+                                        "decomposition": [list(dec_p[0]), dec_p[1]], "wall_s": wall}
+            t1 = scaling["P"].get("1", {}).get("median_epoch_s")
+            for P, e in scaling["P"].items():
+                e["strong_scaling_eff"] = t1 / (int(P) * e["median_epoch_s"]) if t1 else None
+        line = dict(base, value=v, ms_per_step=t * 1e3, iters_per_s=1.0 / t,
+                    config={"workload": f"{'2D' if cfgd['kind'] == '2d' else '3D'} cylinder-wake strong-scaling "
+                                        f"config {args.config}, P=1, N_pde={args.n_pde} (all points, unsampled), "
+                                        f"N_obs={d.n_obs}, reference CPU implementation (flowrec, f64)",
+                            "config_id": args.config, "decomposition": [list(dec[0]), dec[1]],
+                            "colloc_per_rank": d.n_colloc},
+                    cpu_baseline={"value": v, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": _cpu_model(),
+                                  "sample": f"unsampled: {args.steps} full P=1 epochs (LocalObjective.epoch over "
+                                            f"{d.n_colloc} collocation points + {d.n_obs} observations, then "
+                                            f"adam_step), median {t:.3f} s/epoch, BLAS threads={cores}",
+                                  "s_per_epoch": t, "epoch_times_s": t_epochs},
+                    e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        if scaling is not None:
+            line["cpu_scaling"] = scaling
+    else:
+        te, wall, dec = _ref_train_epoch_time(cfgd, world, args.n_pde, args.warmup + args.steps)
+        v = args.n_pde / te
+        line = dict(base, value=v, ms_per_step=te * 1e3, iters_per_s=1.0 / te,
+                    config={"workload": f"cylinder-wake strong-scaling config {args.config}, P={world}, "
+                                        f"N_pde={args.n_pde} global (unsampled), reference process backend",
+                            "config_id": args.config, "decomposition": [list(dec[0]), dec[1]]},
+                    cpu_baseline={"value": v, "unit": UNIT, "cores": world, "kind": kind, "cpu_model": _cpu_model(),
+                                  "host_cores": cores,
+                                  "sample": f"unsampled: train(plan, backend='process') at P={world}, "
+                                            f"{args.warmup + args.steps} epochs, one core per rank, "
+                                            f"TrainResult.median_epoch_time() = {te:.3f} s"},
+                    e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
 
 
@@ -660,6 +786,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-scaling", action="store_true",
+                    help="reference arm: skip the P=1/2/4/8 process-backend scaling column")
+    ap.add_argument("--cpu-scaling-epochs", type=int, default=2)
     args = ap.parse_args()
     if args.n_pde is None:
         args.n_pde = CONFIGS[args.config]["n_pde"]

@@ -136,6 +136,9 @@ typedef struct {
   unsigned timeout_ms;
 } fr_epoch_gate;
 
+/* gate == NULL, or a gate whose `gate` word is NULL: nothing waits; the latter
+ * still applies max_ctas (ungated epochs of a trainer whose workspace was sized
+ * with a cap must launch the same grid). */
 int fr_epoch_workspace_capped(const fr_plan* plan, long long n_colloc, const long long* n_sets, int n_set_count,
                               int max_ctas, fr_workspace* out);
 int fr_epoch_fwd_bwd_gated(const fr_plan* plan, const void* kparams, const void* colloc, long long n_colloc,
@@ -200,7 +203,9 @@ typedef struct {
    * math); history and grad_norm rows use the same index r */
   const double* sched;
   long long row_base;
-  double beta1, beta2, eps, clip_norm; /* clip_norm <= 0: no clipping */
+  double beta1, beta2, eps, clip_norm; /* NaN: no clipping (the reference's None); otherwise
+                                        the gradient is scaled by clip_norm / norm whenever
+                                        norm > clip_norm (optim.py:26-27) */
   /* squared-norm partials written by fr_reduce_grad (NULL: reduce grad here) */
   const double* norm_parts;
   int n_norm_parts;

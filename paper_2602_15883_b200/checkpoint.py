@@ -130,13 +130,14 @@ _FRTS = np.dtype([("magic", "S4"), ("version", "<u4"), ("rank", "<u4"), ("n_para
 
 def save_training_state(path, worker):
     """Device buffers of one RankWorker -> FRTS file (params, Adam m/v, step,
-    epoch counter, history rows, ghost targets)."""
+    epoch counter, history rows, ghost targets; version 2 adds the derivative
+    targets of the opt-in C^1 coupling after each set's (u, p))."""
     import torch
 
     torch.cuda.synchronize()
     worker.sync_history()
     head = np.zeros((), dtype=_FRTS)
-    head["magic"], head["version"], head["rank"] = b"FRTS", 1, worker.rank
+    head["magic"], head["version"], head["rank"] = b"FRTS", 2, worker.rank
     head["n_params"] = worker.flat.numel()
     head["step"] = int(worker.step.item())
     head["epochs_done"] = worker.epochs_done
@@ -144,10 +145,14 @@ def save_training_state(path, worker):
     hist = np.asarray(worker.history, dtype=np.float64).reshape(-1, 7)
     head["n_history"] = hist.shape[0]
     targets = []
-    for gi in range(len(worker.ws.datasets.ghosts)):
+    n_sets = len(worker.ws.datasets.ghosts)
+    for gi in range(n_sets):
         tu, tp = worker.objective.target_slice(gi)
         targets += [tu.double().cpu().numpy().astype("<f8"), tp.double().cpu().numpy().astype("<f8")]
-    head["n_ghost_sets"] = len(targets) // 2
+        tdu = worker.objective.target_du_slice(gi)
+        if tdu is not None:
+            targets.append(tdu.double().cpu().numpy().astype("<f8"))
+    head["n_ghost_sets"] = n_sets
     with open(path, "wb") as f:
         f.write(head.tobytes())
         for t in (worker.flat, worker.m, worker.v):
@@ -166,7 +171,8 @@ def load_training_state(path, worker):
     with open(path, "rb") as f:
         data = f.read()
     head = np.frombuffer(data[: _FRTS.itemsize], dtype=_FRTS)[0]
-    if bytes(head["magic"]) != b"FRTS" or int(head["version"]) != 1:
+    version = int(head["version"])
+    if bytes(head["magic"]) != b"FRTS" or version not in (1, 2):
         raise ValueError(f"{path} is not a training-state file")
     n = int(head["n_params"])
     if int(head["rank"]) != worker.rank or n != worker.flat.numel():
@@ -196,6 +202,11 @@ def load_training_state(path, worker):
         tu, tp = worker.objective.target_slice(gi)
         tu.copy_(torch.as_tensor(take(tu.numel(), tuple(tu.shape)), device=dev))
         tp.copy_(torch.as_tensor(take(tp.numel()), device=dev))
+        tdu = worker.objective.target_du_slice(gi)
+        if tdu is not None:
+            if version < 2:
+                raise ValueError(f"{path} predates derivative targets; cannot resume a C^1-coupled worker")
+            tdu.copy_(torch.as_tensor(take(tdu.numel(), tuple(tdu.shape)), device=dev))
     if int(head["n_ghost_sets"]):
         worker.objective.mark_targets_set()
     prepare(worker.plan, worker.flat, worker.kp)

@@ -78,6 +78,9 @@ struct fr_plan {
 extern "C" const char* fr_last_error(void) { return g_err.c_str(); }
 extern "C" const char* fr_version(void) { return "flowrec_b200 0.1.0 sm_100a"; }
 
+static int preload_capi_kernels();  // defined at the end of this file
+extern "C" int fr_plan_destroy(fr_plan* p);
+
 static int regime_dims(int regime, int* din, int* nout, int* nvel) {
   switch (regime) {
     case FR_STEADY2D: *din = 2; *nout = 3; *nvel = 2; return 0;
@@ -193,6 +196,15 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
     cudaFree(p->d_mapT);
     delete p;
     return cuda_fail(e, "fr_plan_create");
+  }
+  // the transport's signal kernel (and the epoch's reductions / optimiser)
+  // must be resident before a gated epoch kernel spins on them: with lazy
+  // module loading (CUDA_MODULE_LOADING=LAZY, the default) a first launch
+  // would otherwise wait for the device to idle.  Once per plan (plans are
+  // per device), not per launch.
+  if (int rc = preload_capi_kernels()) {
+    fr_plan_destroy(p);
+    return rc;
   }
   *out = p;
   return 0;
@@ -535,16 +547,10 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
   if (!p || !kparams || !colloc || n_colloc < 1 || !gpart || !lpart_blocks || !scratch || n_set_count < 0 ||
       n_set_count > 3 || (n_set_count && !sets))
     return fail("fr_epoch_fwd_bwd: bad arguments");
-  if (gate && (!gate->gate || gate->first_gated_set < 0 || gate->max_ctas < 0))
-    return fail("fr_epoch_fwd_bwd_gated: bad gate");
+  // a gate with a NULL word only caps the grid (ungated epochs of a trainer whose
+  // workspace was sized with fr_epoch_workspace_capped must launch the same grid)
+  if (gate && (gate->first_gated_set < 0 || gate->max_ctas < 0)) return fail("fr_epoch_fwd_bwd_gated: bad gate");
   if (gate && p->info.width_pad > 64) return fail("fr_epoch_fwd_bwd_gated: fused epoch path only (width <= 64)");
-  if (gate) {
-    // the transport's signal kernel must be resident before a kernel that spins
-    // on it is running: with lazy module loading (CUDA_MODULE_LOADING=LAZY, the
-    // default) its first launch would otherwise wait for the device to idle
-    cudaFuncAttributes fa;
-    FR_CUDA(cudaFuncGetAttributes(&fa, signal_kernel), "fr_epoch_fwd_bwd_gated: preload fr_signal");
-  }
   long long ns[3] = {0, 0, 0};
   for (int i = 0; i < n_set_count; ++i) {
     if (sets[i].n < 0 || (sets[i].n > 0 && (!sets[i].pts || !sets[i].target_u)))
@@ -586,7 +592,7 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
     e.mse[i].coef = sets[i].vel_coef;
     e.mse[i].pcoef = sets[i].p_coef;
     e.mse[i].lpart = lpart_blocks[1 + i];
-    if (gate && i >= gate->first_gated_set) {
+    if (gate && gate->gate && i >= gate->first_gated_set) {
       e.mse[i].gate = gate->gate;
       e.mse[i].flags = gate->flags;
       e.mse[i].gate_timeout_ns = (unsigned long long)(gate->timeout_ms ? gate->timeout_ms : 60000u) * 1000000ull;
@@ -817,7 +823,9 @@ __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, co
   // ---- update (optim.py:31-49) ----
   const int i = blockIdx.x * ADAM_NT + tid;
   if (!skip && i < n) {
-    const double scale = (a.clip_norm > 0.0 && norm > a.clip_norm) ? a.clip_norm / norm : 1.0;
+    // clip_by_global_norm: `clip_norm is not None and norm > clip_norm`; None is
+    // NaN here, so the comparison is false (optim.py:26-27)
+    const double scale = (norm > a.clip_norm) ? a.clip_norm / norm : 1.0;
     const double lr = a.sched[3 * row];
     const double bc1 = a.sched[3 * row + 1];
     const double bc2 = a.sched[3 * row + 2];
@@ -1024,5 +1032,20 @@ extern "C" int fr_bench_ffma(int grid, int iters, int, float* out, fr_stream_t s
   ffma_kernel<<<grid, 256, 0, stream>>>(iters, out);
   ++g_kernel_launches;
   FR_CUDA(cudaGetLastError(), "fr_bench_ffma");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+static int preload_capi_kernels() {
+  cudaFuncAttributes fa;
+  FR_CUDA(cudaFuncGetAttributes(&fa, signal_kernel), "preload fr_signal");
+  FR_CUDA(cudaFuncGetAttributes(&fa, reduce_grad_kernel), "preload fr_reduce_grad");
+  FR_CUDA(cudaFuncGetAttributes(&fa, reduce_loss_kernel), "preload fr_reduce_loss");
+  FR_CUDA(cudaFuncGetAttributes(&fa, adam_kernel<float>), "preload fr_adam_step");
+  FR_CUDA(cudaFuncGetAttributes(&fa, adam_kernel<double>), "preload fr_adam_step");
+  FR_CUDA(cudaFuncGetAttributes(&fa, pack_ghost_kernel<float>), "preload fr_pack_ghost");
+  FR_CUDA(cudaFuncGetAttributes(&fa, pack_ghost_kernel<double>), "preload fr_pack_ghost");
+  FR_CUDA(cudaFuncGetAttributes(&fa, prepare_kernel<float>), "preload fr_prepare_params");
+  FR_CUDA(cudaFuncGetAttributes(&fa, prepare_kernel<double>), "preload fr_prepare_params");
   return 0;
 }

@@ -14,6 +14,29 @@ struct KInfo {
   int cps = 1;       // epoch kernel: resident CTAs per SM (persistent grid = SMs x cps)
 };
 
+// Load a kernel and set its shared-memory attributes once per device, at plan /
+// workspace time.  With lazy module loading (the CUDA 12 default) a kernel's
+// first launch waits for the device to go idle; a gated epoch kernel whose
+// first launch sits behind a still-running transport would then wait for the
+// transport to finish instead of overlapping it (and its exchange timeout would
+// never fire).  `loaded` is a per-kernel-instance bitmask of device ordinals.
+template <typename K>
+int ensure_loaded(K k, size_t smem, bool carveout, unsigned long long& loaded) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return int(e);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&loaded, __ATOMIC_ACQUIRE) & bit) return 0;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, k);  // forces the module load
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  // all of the unified L1/shared array as shared memory, so the resident CTAs fit
+  if (e == cudaSuccess && carveout) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return int(e);
+  __atomic_fetch_or(&loaded, bit, __ATOMIC_RELEASE);
+  return 0;
+}
+
 template <int V>
 struct IntC {
   static constexpr int value = V;
@@ -44,16 +67,18 @@ int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
     info->stash_elems = C::NT * C::stash_per_thread(L);
     info->smem = smem;
   }
-  if (!a) return 0;
   auto k = jetmlp_kernel<T, ACT, MODE, REG, W>;
-  // raise the opt-in shared-memory limit once (not a stream operation, but kept
-  // out of the steady state so that captured epochs only contain launches)
+  // load + raise the opt-in shared-memory limit once per device (not a stream
+  // operation: kept out of the steady state so captured epochs only contain
+  // launches); every workspace query does it, before any launch
+  static unsigned long long loaded = 0;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return int(e);
+    loaded = 0;  // a larger L needs the attribute raised again
     smem_set = smem;
   }
+  if (int r = ensure_loaded(k, smem_set, false, loaded)) return r;
+  if (!a) return 0;
   k<<<grid, C::NT, smem, st>>>(*a);
   ++g_kernel_launches;
   return int(cudaGetLastError());
@@ -74,17 +99,15 @@ int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L)
     info->smem = smem;
     info->cps = E::CPS;
   }
-  if (!e) return 0;
   auto k = jetmlp_epoch_kernel<T, ACT, REG, W>;
+  static unsigned long long loaded = 0;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (err != cudaSuccess) return int(err);
-    // all of the unified L1/shared array as shared memory, so E::CPS CTAs fit
-    err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (err != cudaSuccess) return int(err);
+    loaded = 0;
     smem_set = smem;
   }
+  if (int r = ensure_loaded(k, smem_set, true, loaded)) return r;
+  if (!e) return 0;
   k<<<grid, CP::NT, smem, st>>>(*e);
   ++g_kernel_launches;
   return int(cudaGetLastError());

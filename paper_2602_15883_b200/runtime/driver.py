@@ -137,8 +137,9 @@ class LocalTrainer:
     the in-kernel wait, not stream order, protects the ghost heads)."""
 
     def __init__(self, plan: TrainingPlan, dtype="float32", epochs=None, overlap=False, reserve_sms=None,
-                 signal_delay_ns=0):
+                 signal_delay_ns=0, exchange_timeout=600.0):
         self.plan = plan
+        self.exchange_timeout = float(exchange_timeout)
         self.overlap = bool(overlap)
         self.signal_delay_ns = int(signal_delay_ns)
         if reserve_sms is None:
@@ -150,7 +151,8 @@ class LocalTrainer:
         if self.overlap:
             self.comm = torch.cuda.Stream()
             self.gates = torch.zeros(len(self.order), dtype=torch.int32, device="cuda")
-            self.gate_args = {r: self.workers[r].objective.make_gate(self.gates[i], self.workers[r].flags)
+            self.gate_args = {r: self.workers[r].objective.make_gate(self.gates[i], self.workers[r].flags,
+                                                                     self.exchange_timeout)
                               for i, r in enumerate(self.order)}
         self.routes = []
         for r in self.order:
@@ -246,6 +248,11 @@ class LocalTrainer:
             # lazily set attribute); later epochs replay captured graphs of the
             # same work
             if use_graphs and self._ran_eager:
+                # a replay bypasses enqueue_epoch's capacity check: the optimiser
+                # kernel indexes the schedule / history rows by its step counter
+                for w in self.workers.values():
+                    if w.epochs_done + block > w.capacity:
+                        raise RuntimeError("history capacity exhausted; construct the trainer with more epochs")
                 self._graph(exchange, block).replay()
             else:
                 self._enqueue(exchange)
@@ -268,9 +275,9 @@ class LocalTrainer:
         return times
 
 
-def _train_local(plan, dtype, use_graphs):
+def _train_local(plan, dtype, use_graphs, exchange_timeout=600.0):
     t0 = time.perf_counter()
-    trainer = LocalTrainer(plan, dtype=dtype)
+    trainer = LocalTrainer(plan, dtype=dtype, exchange_timeout=exchange_timeout)
     trainer.run(plan.train_config.epochs, use_graphs=use_graphs)
     return _collect(plan, {r: w.export() for r, w in trainer.workers.items()}, time.perf_counter() - t0)
 
@@ -361,7 +368,7 @@ class DistributedTrainer:
     synchronise the device)."""
 
     def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=None,
-                 transport="torch"):
+                 transport="torch", exchange_timeout=600.0):
         import torch.distributed as dist
 
         if transport not in ("torch", "fr_nccl"):
@@ -399,7 +406,9 @@ class DistributedTrainer:
         if self.overlap:
             self.comm = torch.cuda.Stream()
             self.gate_word = torch.zeros(1, dtype=torch.int32, device=dev)
-            self.gate = w.objective.make_gate(self.gate_word, w.flags)
+            # the in-kernel wait is bounded by the reference's exchange timeout
+            # (driver.py:150-181): a lost peer -> FLAG_EXCHANGE_TIMEOUT -> DeadlockError
+            self.gate = w.objective.make_gate(self.gate_word, w.flags, exchange_timeout)
 
     def _du(self, k):
         b = self.send_bufs[k]
@@ -459,25 +468,25 @@ class DistributedTrainer:
         return times
 
 
-def _train_distributed(plan, dtype):
+def _train_distributed(plan, dtype, exchange_timeout=600.0):
     import torch.distributed as dist
 
     t0 = time.perf_counter()
-    tr = DistributedTrainer(plan, dtype=dtype)
+    tr = DistributedTrainer(plan, dtype=dtype, exchange_timeout=exchange_timeout)
     tr.run(plan.train_config.epochs)
     exports = [None] * plan.n_ranks
     dist.all_gather_object(exports, (tr.rank, tr.worker.export()))
     return _collect(plan, dict(exports), time.perf_counter() - t0)
 
 
-def _process_entry(local_rank, plan, dtype, port, q):
+def _process_entry(local_rank, plan, dtype, port, q, exchange_timeout=600.0):
     import torch.distributed as dist
 
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", rank=local_rank, world_size=plan.n_ranks)
-        res = _train_distributed(plan, dtype)
+        res = _train_distributed(plan, dtype, exchange_timeout)
         if local_rank == 0:
             q.put(("ok", res))
         dist.destroy_process_group()
@@ -495,7 +504,7 @@ def _train_process(plan, dtype, timeout):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + os.getpid() % 1000
-    procs = [ctx.Process(target=_process_entry, args=(r, plan, dtype, port, q), daemon=True)
+    procs = [ctx.Process(target=_process_entry, args=(r, plan, dtype, port, q, timeout), daemon=True)
              for r in range(plan.n_ranks)]
     for p in procs:
         p.start()
@@ -526,10 +535,12 @@ def _collect(plan, exports, wall):
 
 def train(plan: TrainingPlan, backend="serial", exchange_timeout=600.0, dtype="float32", use_graphs=True):
     """Run the distributed training loop on the GPU(s)."""
+    if not exchange_timeout > 0:
+        raise ValueError("exchange timeout must be positive")
     if backend in ("serial", "cuda"):
-        return _train_local(plan, dtype, use_graphs)
+        return _train_local(plan, dtype, use_graphs, exchange_timeout)
     if backend == "distributed":
-        return _train_distributed(plan, dtype)
+        return _train_distributed(plan, dtype, exchange_timeout)
     if backend == "process":
         return _train_process(plan, dtype, exchange_timeout)
     raise ValueError(f"unknown backend {backend!r} (use 'serial', 'cuda', 'distributed' or 'process')")

@@ -26,6 +26,18 @@ SEG_OBS, SEG_PDE, SEG_GS, SEG_GT = 0, 1, 2, 3
 KINDS = ("spatial", "temporal")
 
 
+def check_finite(name, arr):
+    """ValueError naming the first non-finite entry, as the reference's tape
+    binding does (autodiff/tape.py:251-255).  The reference checks each
+    shuffled mini-batch as it binds it, so its index is batch-relative; here
+    every dataset is checked once, whole, at upload, and the index is the
+    dataset row."""
+    a = arr.detach().cpu().numpy() if torch.is_tensor(arr) else np.asarray(arr, dtype=np.float64)
+    if not np.all(np.isfinite(a)):
+        idx = tuple(int(i) for i in np.argwhere(~np.isfinite(a))[0])
+        raise ValueError(f"non-finite value in {name} at index {idx}")
+
+
 class DeviceObjective:
     """Resident datasets, workspaces and the per-epoch launch sequence."""
 
@@ -52,6 +64,14 @@ class DeviceObjective:
             raise ValueError(f"need one velocity weight per component ({nv}), got {len(vw)}")
         self.vel_w = (ctypes.c_double * 4)(*(list(vw) + [1.0] * (4 - nv)))
 
+        # the reference validates every input it binds (tape.py:298-313); the
+        # datasets are resident here, so they are checked once
+        check_finite("input 'points'", datasets.colloc_points)
+        if self.n_obs:
+            check_finite("input 'points'", datasets.obs_points)
+            check_finite("input 'target_u'", datasets.obs_velocity)
+        for g in datasets.ghosts:
+            check_finite("input 'points'", g.points)
         self.obs_pts = to_device(datasets.obs_points.reshape(-1, regime.n_inputs), T, dev)
         self.obs_vel = to_device(datasets.obs_velocity.reshape(-1, nv), T, dev)
         self.col_pts = to_device(datasets.colloc_points, T, dev)
@@ -127,6 +147,8 @@ class DeviceObjective:
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
         # ghost sets follow obs in set_order: the overlapped exchange gates them
         self.first_ghost_set = 1 if self.n_obs else 0
+        # ungated launches of a capped workspace still launch the capped grid
+        self.cap_gate = X.EpochGate(None, 0, self.max_ctas, None, 0) if self.max_ctas else None
 
     def _init_ghost_derivatives(self, plan, epoch_rows, npad, dev):
         """Extension buffers: per ghost kind the derivative targets (N, n_in,
@@ -153,12 +175,17 @@ class DeviceObjective:
         self.total_rows = rows
         self.gpart = torch.empty(rows * npad, dtype=torch.float64, device=dev)
 
-    def make_gate(self, gate_word, flags, timeout_ms=60000):
-        """fr_epoch_gate for the overlapped exchange (ghost sets wait on gate_word)."""
+    def make_gate(self, gate_word, flags, timeout_s=600.0):
+        """fr_epoch_gate for the overlapped exchange (ghost sets wait on
+        gate_word for at most timeout_s: the reference's exchange_timeout,
+        driver.py:150-181, 259)."""
         if self.wide:
             raise ValueError("the overlapped exchange needs the fused epoch kernel (hidden width <= 64)")
+        if not timeout_s > 0:
+            raise ValueError("exchange timeout must be positive")
+        timeout_ms = min(int(round(float(timeout_s) * 1000.0)), 2**32 - 1)
         return X.EpochGate(gate_word.data_ptr(), self.first_ghost_set, self.max_ctas, flags.data_ptr(),
-                           int(timeout_ms))
+                           max(timeout_ms, 1))
 
     def _init_wide(self, plan, counts, weights, dev):
         """Wide experts (hidden width > 64): one layer-wise launch sequence per
@@ -246,6 +273,11 @@ class DeviceObjective:
             p_t = p if torch.is_tensor(p) else torch.as_tensor(np.asarray(p, dtype=np.float64))
             if tuple(u_t.shape) != (n, nv) or tuple(p_t.shape) != (n,):
                 raise ValueError("ghost target shape mismatch")
+            # the reference binds the targets as tape inputs (tape.py:298-313)
+            check_finite("input 'target_u'", u_t)
+            check_finite("input 'target_p'", p_t)
+            if du is not None:
+                check_finite("input 'target_du'", du_t)
             tu, tp = self.target_slice(gi)
             tu.copy_(u_t)
             tp.copy_(p_t)
@@ -281,7 +313,8 @@ class DeviceObjective:
             X.call("fr_epoch_fwd_bwd_gated", plan.h, X.ptr(kparams), X.ptr(self.col_pts), self.n_colloc,
                    self.weights.pde / self.n_colloc, self.sets, len(self.set_order), self.vel_w,
                    X.ptr(self.gpart), self.lpart_blocks, X.ptr(self.scratch),
-                   ctypes.byref(gate) if gate is not None else None, st)
+                   ctypes.byref(gate if gate is not None else self.cap_gate)
+                   if (gate is not None or self.cap_gate is not None) else None, st)
         npad = plan.info.np_pad
         for kind, n, grow, lrow, _ in self.gd_launches:
             g = self.ghost[kind]
@@ -339,6 +372,17 @@ class LocalObjective:
         flat = params.flat if hasattr(params, "flat") else np.asarray(params, dtype=np.float64)
         flat_d = to_device(flat, torch.float64, self.plan.device)
         if not torch.isfinite(flat_d).all():
+            # the reference reports the index inside the offending tape array
+            # (W0, b0, W1, ... ; tape.py:314-326)
+            bad = int(torch.nonzero(~torch.isfinite(flat_d))[0])
+            off = 0
+            for wshape, bshape in self.config.layer_shapes:
+                for shp in (wshape, bshape):
+                    size = int(np.prod(shp))
+                    if bad < off + size:
+                        idx = tuple(int(i) for i in np.unravel_index(bad - off, shp))
+                        raise ValueError(f"non-finite value in parameter at index {idx}")
+                    off += size
             raise ValueError("non-finite value in parameter")
         prepare(self.plan, flat_d, self._kp)
         self.dev.enqueue(self._kp)

@@ -42,38 +42,38 @@ class AdamState:
         return cls(m=z(), v=z())
 
 
-_counters = {}
-
-
-def _sync_counter(device):
-    """Zero-initialised device int for the optimiser's last-block step update
-    (self-resetting, so one per device is enough for any number of calls)."""
-    c = _counters.get(device)
-    if c is None:
-        c = torch.zeros(1, dtype=torch.int32, device=device)
-        _counters[device] = c
-    return c
+def new_sync_counter(device):
+    """Zero-initialised device int for the optimiser's last-block step update.
+    It self-resets after every launch, but launches that may run concurrently
+    (workers on different streams of one GPU) each need their own."""
+    return torch.zeros(1, dtype=torch.int32, device=device)
 
 
 def launch_adam(params, grad, m, v, step, sched, row_base, *, beta1=0.9, beta2=0.999, eps=1e-8,
                 clip_norm=None, flags, grad_norm=None, plan=None, kparams=None, history=None,
-                loss=None, norm_parts=None, stream=None):
+                loss=None, norm_parts=None, stream=None, sync_counter=None):
     """Enqueue fr_adam_step on device tensors (graph-capturable).
 
-    loss: None or dict(lpart=<tensor>, seg_rows=[4 ints], n_obs=..., w_obs=..., ...)."""
+    loss: None or dict(lpart=<tensor>, seg_rows=[4 ints], n_obs=..., w_obs=..., ...).
+    sync_counter: this caller's counter (new_sync_counter); None allocates a
+    fresh one, which a graph-captured or repeated caller must not rely on."""
     a = X.AdamArgs()
     a.n = params.numel()
     a.params, a.grad, a.m, a.v = (t.data_ptr() for t in (params, grad, m, v))
     a.step, a.sched, a.row_base = step.data_ptr(), sched.data_ptr(), int(row_base)
     a.beta1, a.beta2, a.eps = float(beta1), float(beta2), float(eps)
-    a.clip_norm = 0.0 if clip_norm is None else float(clip_norm)
+    # None -> NaN: the kernel's `norm > clip_norm` is then false, as the
+    # reference's `clip_norm is not None and norm > clip_norm` (optim.py:26)
+    a.clip_norm = float("nan") if clip_norm is None else float(clip_norm)
     if norm_parts is not None:
         a.norm_parts, a.n_norm_parts = norm_parts.data_ptr(), norm_parts.numel()
     a.flags = flags.data_ptr()
     a.grad_norm = None if grad_norm is None else grad_norm.data_ptr()
     a.kparams = None if kparams is None else kparams.data_ptr()
     a.history = None if history is None else history.data_ptr()
-    a.sync_counter = _sync_counter(params.device).data_ptr()
+    if sync_counter is None:
+        sync_counter = new_sync_counter(params.device)
+    a.sync_counter = sync_counter.data_ptr()
     for k, val in (loss or {}).items():
         if k == "lpart":
             a.lpart = val.data_ptr()

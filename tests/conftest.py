@@ -40,3 +40,26 @@ def max_rel(a, b, floor=1e-300):
     b = np.asarray(b, dtype=np.float64)
     scale = max(float(np.max(np.abs(a))), float(np.max(np.abs(b))), floor)
     return float(np.max(np.abs(a - b))) / scale
+
+
+def report(tag, **errors):
+    """Print measured parity errors (visible with -s) and, when FR_PARITY_LOG
+    names a file, append them as one JSON line (profiles/ keeps the record)."""
+    import json
+
+    line = {"test": tag, **{k: float(v) for k, v in errors.items()}}
+    print("parity", json.dumps(line))
+    path = os.environ.get("FR_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(line) + "\n")
+
+
+def per_term_rel(a, b, floor=0.0):
+    """max_i |a_i - b_i| / |b_i| over entries with |b_i| > floor."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    m = np.abs(b) > floor
+    if not m.any():
+        return float(np.max(np.abs(a - b), initial=0.0))
+    return float(np.max(np.abs(a[m] - b[m]) / np.abs(b[m])))

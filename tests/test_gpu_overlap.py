@@ -59,7 +59,7 @@ def test_gate_timeout_flags_deadlock(golden):
     w = RankWorker(plan.worker_specs[0], max_ctas=8)
     w.objective.mark_targets_set()
     gate_word = torch.zeros(1, dtype=torch.int32, device="cuda")
-    gate = w.objective.make_gate(gate_word, w.flags, timeout_ms=20)
+    gate = w.objective.make_gate(gate_word, w.flags, timeout_s=0.02)
     w.enqueue_epoch(gate=gate)
     torch.cuda.synchronize()
     assert int(w.flags.item()) & X.FLAG_EXCHANGE_TIMEOUT

@@ -169,3 +169,35 @@ def test_evaluation_ownership_bit_exact(tag, kind, counts, m):
                           g[f"{tag}/points"])
     anchor = tuple(g[f"{tag}/anchor"])
     assert sorted(identify_masters(subs, anchor)) == [int(r) for r in g[f"{tag}/masters"]]
+
+
+def test_check_finite_reports_reference_message():
+    """tape.py:251-255: 'non-finite value in <name> at index <tuple>'."""
+    from paper_2602_15883_b200.runtime.objective import check_finite
+
+    a = np.zeros((4, 3))
+    check_finite("input 'points'", a)
+    a[2, 1] = np.nan
+    with pytest.raises(ValueError, match=r"non-finite value in input 'points' at index \(2, 1\)"):
+        check_finite("input 'points'", a)
+
+
+def test_headline_inputs_bit_exact_with_reference():
+    """The benchmarked config's datasets (500k P=1; 20k (2,2)x2) regenerate
+    bit-exactly: SHA-256 of the reference's arrays (golden_headline.npz)."""
+    import hashlib
+
+    from paper_2602_15883_b200 import config as fconfig
+
+    hg = np.load(os.path.join(ROOT, "tests", "golden", "golden_headline.npz"))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()  # noqa: E731
+    pb = fconfig.cylinder2d_problem(n_procs=1)
+    assert sha(pb.datasets[0].colloc_points) == str(hg["full/colloc_sha"])
+    assert sha(pb.datasets[0].obs_points) == str(hg["full/obs_sha"])
+    pb8 = fconfig.cylinder2d_problem(n_pde=20_000, counts=(2, 2), time_splits=2)
+    for r in (0, 3):
+        d = pb8.datasets[r]
+        assert sha(d.colloc_points) == str(hg[f"ep/{r}/colloc_sha"])
+        assert np.array_equal(d.obs_points, hg[f"ep/{r}/obs_points"])
+        for gi, g in enumerate(d.ghosts):
+            assert np.array_equal(g.points, hg[f"ep/{r}/ghost{gi}"])

@@ -91,3 +91,28 @@ def test_oracle_serial_training_matches_reference(golden, tag):
     for r in ranks:
         assert rel_l2(hist[r], golden[f"{tag}/r{r}/history"]) < 1e-11, r
         assert rel_l2(ranks[r]["flat"], golden[f"{tag}/r{r}/final"]) < 1e-12, r
+
+
+@pytest.mark.parametrize("rank", [0, 3])
+def test_oracle_headline_epoch_matches_reference(rank):
+    """The oracle on the benchmarked network: LocalObjective.epoch of a master
+    and a slave rank of (2,2)x2 with spatial + temporal ghosts
+    (golden_headline.npz, written by the reference)."""
+    import os
+
+    from conftest import ROOT
+    from paper_2602_15883_b200 import config as fconfig
+
+    hg = np.load(os.path.join(ROOT, "tests", "golden", "golden_headline.npz"))
+    pb = fconfig.cylinder2d_problem(n_pde=20_000, counts=(2, 2), time_splits=2)
+    d = pb.datasets[rank]
+    k = f"ep/{rank}"
+    w = hg[f"{k}/weights"]
+    ghosts = [(g.kind, g.points, hg[f"{k}/ghost{gi}_u"], hg[f"{k}/ghost{gi}_p"]) for gi, g in enumerate(d.ghosts)]
+    parts, grad, total = O.local_epoch(
+        hg[f"{k}/params"], pb.expert_config.arch, "tanh", "unsteady2d", 100.0,
+        dict(obs_pts=d.obs_points, obs_vel=d.obs_velocity, colloc=d.colloc_points, ghosts=ghosts),
+        dict(obs=w[0], pde=w[1], ghost_u=w[2], ghost_p_space=w[3], ghost_p_time=w[4], velocity=None))
+    assert max_rel(parts, hg[f"{k}/parts"]) < 1e-12
+    assert abs(total - float(hg[f"{k}/total"])) <= 1e-12 * abs(total)
+    assert rel_l2(grad, hg[f"{k}/grad"]) < 1e-11
