@@ -17,7 +17,7 @@ from conftest import max_rel, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-F32_LOSS, F32_GRAD = 2e-5, 1e-4
+F32_LOSS, F32_GRAD = 1e-5, 1e-5
 
 
 @pytest.fixture(scope="module")

@@ -9,17 +9,19 @@ Two builds of the same kernel templates are checked:
 import numpy as np
 import pytest
 
-from conftest import max_rel, rel_l2
+from conftest import max_rel, rel_l2, report
 
 pytestmark = pytest.mark.gpu
 
 KINDS = {0: "steady2d", 1: "unsteady2d", 2: "unsteady3d"}
 RE = {}
 
-# stated FP32 tolerances (relative): jets / losses / gradients
-F32_JET = 2e-5
-F32_LOSS = 2e-5
-F32_GRAD = 1e-4
+# stated FP32 tolerances (relative): jets (value, gradient and
+# Laplacian streams, max-abs relative to the largest entry) / losses /
+# gradients (norm-wise) -- measured errors are <= 1.1e-6 (profiles/r2_parity_errors.jsonl)
+F32_JET = 1e-5
+F32_LOSS = 1e-5
+F32_GRAD = 1e-5
 # stated TF32 tensor-core tolerances (wide FP32 experts, relative): one TF32
 # rounding (2^-11) per product, accumulated in FP32 through the layer chain
 TF32_LOSS = 5e-3
@@ -49,11 +51,12 @@ def test_jet_forward(golden, i, dtype):
     d = cfg.input_dim
     val, grad, lap = y[:, 0], np.transpose(y[:, 1 : 1 + d], (0, 2, 1)), np.transpose(y[:, 1 + d :], (0, 2, 1))
     tol = 1e-12 if dtype == "float64" else F32_JET
-    assert max_rel(val, golden[f"{t}/jet_value"]) < tol
-    assert max_rel(grad, golden[f"{t}/jet_grad"]) < tol * 10
-    assert max_rel(lap, golden[f"{t}/jet_lap"]) < tol * 10
     v = engine.forward_values(plan, golden[f"{t}/params"], golden[f"{t}/pts"])
-    assert max_rel(v, golden[f"{t}/jet_value"]) < tol
+    e = dict(value=max_rel(val, golden[f"{t}/jet_value"]), grad=max_rel(grad, golden[f"{t}/jet_grad"]),
+             lap=max_rel(lap, golden[f"{t}/jet_lap"]), predict=max_rel(v, golden[f"{t}/jet_value"]))
+    report(f"jet/{t}/{dtype}", **e)
+    assert e["value"] < tol and e["predict"] < tol
+    assert e["grad"] < tol and e["lap"] < tol
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
@@ -66,8 +69,10 @@ def test_pde_loss_and_gradient(golden, i, dtype):
     sq, g = engine.pde_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], float(meta[3]))
     ref_sq = float(golden[f"{t}/sq_pde"])
     tol_l, tol_g = (1e-11, 1e-10) if dtype == "float64" else (F32_LOSS, F32_GRAD)
-    assert abs(sq - ref_sq) <= tol_l * abs(ref_sq), (sq, ref_sq)
-    assert rel_l2(g, golden[f"{t}/grad_pde"]) < tol_g
+    e_l, e_g = abs(sq - ref_sq) / abs(ref_sq), rel_l2(g, golden[f"{t}/grad_pde"])
+    report(f"pde/{t}/{dtype}", loss=e_l, grad=e_g)
+    assert e_l <= tol_l, (sq, ref_sq)
+    assert e_g < tol_g
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
@@ -81,9 +86,11 @@ def test_mse_loss_and_gradient(golden, i, dtype):
     su, sp, g = engine.mse_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], golden[f"{t}/tu"],
                                      golden[f"{t}/tp"], list(meta[6 : 6 + nv]), float(meta[4]), float(meta[5]))
     tol_l, tol_g = (1e-12, 1e-11) if dtype == "float64" else (F32_LOSS, F32_GRAD)
-    assert abs(su - float(golden[f"{t}/sq_u"])) <= tol_l * abs(su)
-    assert abs(sp - float(golden[f"{t}/sq_p"])) <= tol_l * abs(sp)
-    assert rel_l2(g, golden[f"{t}/grad_mse"]) < tol_g
+    e = dict(sq_u=abs(su - float(golden[f"{t}/sq_u"])) / abs(su), sq_p=abs(sp - float(golden[f"{t}/sq_p"])) / abs(sp),
+             grad=rel_l2(g, golden[f"{t}/grad_mse"]))
+    report(f"mse/{t}/{dtype}", **e)
+    assert e["sq_u"] <= tol_l and e["sq_p"] <= tol_l
+    assert e["grad"] < tol_g
 
 
 def test_rerun_bit_identical(golden):
@@ -131,6 +138,7 @@ def test_f32_matches_oracle_at_cylinder_scale(act):
     sq_ref, g_ref, _ = O.pde_loss_grad(p, cfg.arch, act, "unsteady2d", 100.0, pts, coef)
     plan = engine.get_plan(cfg, "unsteady2d", 100.0, "float32")
     sq, g = engine.pde_loss_grad(plan, p, pts, coef)
+    report(f"cylinder_scale/{act}", loss=abs(sq - sq_ref) / sq_ref, grad=rel_l2(g, g_ref))
     assert abs(sq - sq_ref) <= F32_LOSS * sq_ref, (sq, sq_ref)
     assert rel_l2(g, g_ref) < F32_GRAD
 

@@ -6,12 +6,15 @@ import numpy as np
 import pytest
 
 from cases import training_plan
-from conftest import max_rel, rel_l2
+from conftest import max_rel, per_term_rel, rel_l2, report
 
 pytestmark = pytest.mark.gpu
 
-F32_HIST = 1e-4
+F32_HIST = 1e-5
 F32_PARAMS = 1e-6
+# per-term losses and the flat gradient within 1e-5 on the SIMT path
+F32_TERM = 1e-5
+F32_GRAD = 1e-5
 # TF32 tensor-core path (wide experts): stated bounds after 3 epochs
 TF32_HIST = 2e-2
 TF32_PARAMS = 1e-3  # Adam normalises updates: TF32 noise on near-zero gradient components moves those params by up to ~lr per step
@@ -42,10 +45,12 @@ def _objective(golden, tag, dtype):
 def test_local_objective_epoch(golden, tag, dtype):
     obj = _objective(golden, tag, dtype)
     parts, grad, total = obj.epoch(golden["obj/params"], None)
-    tol_p, tol_g = (1e-11, 1e-10) if dtype == "float64" else (2e-5, 1e-4)
-    assert max_rel(parts.astuple(), golden[f"{tag}/parts"]) < tol_p
-    assert abs(total - float(golden[f"{tag}/total"])) <= tol_p * abs(total)
-    assert rel_l2(grad, golden[f"{tag}/grad"]) < tol_g
+    tol_p, tol_g = (1e-11, 1e-10) if dtype == "float64" else (F32_TERM, F32_GRAD)
+    e = dict(term=per_term_rel(parts.astuple(), golden[f"{tag}/parts"]),
+             total=abs(total - float(golden[f"{tag}/total"])) / abs(total), grad=rel_l2(grad, golden[f"{tag}/grad"]))
+    report(f"local_objective/{tag}/{dtype}", **e)
+    assert e["term"] < tol_p and e["total"] <= tol_p
+    assert e["grad"] < tol_g
 
 
 def test_master_reports_spatial_pressure_loss(golden):
@@ -85,12 +90,17 @@ def test_training_matches_reference_serial_driver(golden, tag, dtype):
     _, plan = training_plan(tag, golden)
     res = train(plan, backend="serial", dtype=dtype)
     tol_h, tol_p = (1e-9, 1e-11) if dtype == "float64" else (F32_HIST, F32_PARAMS)
+    worst_h = worst_p = 0.0
     for r in res.params:
         h, ref_h = res.history[r], golden[f"{tag}/r{r}/history"]
         assert h.shape == ref_h.shape
         assert np.array_equal(h[:, 0], ref_h[:, 0]) and np.array_equal(h[:, 6], ref_h[:, 6])
-        assert max_rel(h[:, 1:6], ref_h[:, 1:6]) < tol_h, (r, h, ref_h)
-        assert rel_l2(res.params[r].flat, golden[f"{tag}/r{r}/final"]) < tol_p, r
+        eh = per_term_rel(h[:, 1:6], ref_h[:, 1:6], floor=1e-300)
+        ep = rel_l2(res.params[r].flat, golden[f"{tag}/r{r}/final"])
+        worst_h, worst_p = max(worst_h, eh), max(worst_p, ep)
+        assert eh < tol_h, (r, h, ref_h)
+        assert ep < tol_p, r
+    report(f"train/{tag}/{dtype}", history_term=worst_h, params=worst_p)
 
 
 def test_graph_replay_bit_identical_to_eager(golden):
