@@ -297,8 +297,10 @@ def run_ours(args):
     # launches per epoch: count library launches while capturing / enqueuing one epoch
     if world == 1:
         lp = _launches_per_epoch(trainer, X)
+    elif getattr(trainer, "launches_per_epoch", None):
+        lp = trainer.launches_per_epoch.get(True)  # IPC transport: kernels in the captured epoch graph
     else:
-        lp = launches_timed / args.steps  # no graphs: the library counted every launch
+        lp = launches_timed / args.steps  # NCCL transports run eagerly: the library counted every launch
 
     # ---- e2e: host pinned inputs copied in + loss row copied out every step ----
     obj = worker.objective

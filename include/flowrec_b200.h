@@ -134,6 +134,11 @@ typedef struct {
   int max_ctas;
   int* flags;
   unsigned timeout_ms;
+  /* peer-memory transport: when gate_round is non-NULL the gate is a monotonic
+   * arrival counter and the ghost sets wait until *gate >= *gate_round * gate_mult
+   * (gate_mult = incoming edges per round; *gate_round = rounds so far) */
+  const unsigned* gate_round;
+  unsigned gate_mult;
 } fr_epoch_gate;
 
 /* gate == NULL, or a gate whose `gate` word is NULL: nothing waits; the latter
@@ -172,6 +177,49 @@ int fr_nccl_destroy(fr_comm* comm);
 int fr_exchange(fr_comm* comm, int n_send, const int* send_peers, const void* const* send_bufs,
                 const long long* send_counts, int n_recv, const int* recv_peers, void* const* recv_bufs,
                 const long long* recv_counts, int dtype, fr_stream_t stream);
+
+/* Peer-memory ghost transport (one process per GPU over NVLink / NVSwitch, or
+ * several ranks in one process).  Each rank allocates its ghost-target rows and
+ * its sync words in one block with fr_ipc_alloc (cudaMalloc + IPC handle of 64
+ * bytes); peers map it with fr_ipc_open (peer access enabled lazily).  The
+ * producer's pack then stores straight into the destination's target rows --
+ * no staging buffer, no NCCL kernel -- so the whole epoch (producer -> put ->
+ * gated epoch kernel -> reductions -> Adam) is one CUDA graph.
+ *
+ * Sync words per rank (u32, monotonic, zero-initialised):
+ *   ready    -- + 1 by every source after its rows for this rank landed
+ *               (release, system scope); the epoch kernel's ghost sets wait
+ *               for ready >= rounds * n_incoming (fr_epoch_gate.gate_round)
+ *   epochs   -- + 1 by the rank itself after each epoch kernel (its targets
+ *               are free again); a source writes round k's rows for an epoch e
+ *               only once the destination's `epochs` has reached e (WAR guard),
+ *               comparing against its own `epochs` word (ranks run the same
+ *               epoch sequence) */
+typedef struct {
+  long long y_row;          /* first row of this edge in the producer's value output y */
+  long long anchor_row;     /* rows of the anchor evaluations (masters), or -1 */
+  long long n;              /* ghost points */
+  void* u;                  /* destination's target rows (n, n_vel), peer pointer */
+  void* p;                  /* (n,) */
+  void* du;                 /* (n, n_in, n_vel) derivative targets or NULL (C^1 extension) */
+  unsigned* ready;          /* destination's ready word (peer pointer) */
+  const unsigned* epochs;   /* destination's epochs word (peer pointer) */
+} fr_ghost_edge;
+#define FR_MAX_GHOST_EDGES 16
+
+int fr_ipc_alloc(size_t bytes, void** ptr, void* handle_out);
+int fr_ipc_open(const void* handle, void** ptr);
+int fr_ipc_close(void* ptr);
+int fr_ipc_free(void* ptr);
+/* One round of this rank's outgoing edges: per edge wait (bounded by timeout_ms;
+ * FR_FLAG_EXCHANGE_TIMEOUT into *flags) until *edge.epochs >= *my_epochs, store
+ * u = y[:, :n_vel], p = y[:, p] - y_anchor[:, p] (anchor-normalised on masters,
+ * worker.py:24-46,170-198) [and du from y_jet (n, 1 + 2 n_in, n_out)] into the
+ * destination, then release-add 1 to *edge.ready. */
+int fr_ghost_put(const fr_plan* plan, const void* y, const void* y_jet, int n_edges, const fr_ghost_edge* edges,
+                 const unsigned* my_epochs, unsigned timeout_ms, int* flags, fr_stream_t stream);
+/* *word += value (release, system scope) once prior work on `stream` is done */
+int fr_counter_add(unsigned* word, unsigned value, fr_stream_t stream);
 
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,

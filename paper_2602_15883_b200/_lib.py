@@ -65,7 +65,18 @@ class AdamArgs(C.Structure):
 
 class EpochGate(C.Structure):
     _fields_ = [("gate", C.c_void_p), ("first_gated_set", C.c_int), ("max_ctas", C.c_int),
-                ("flags", C.c_void_p), ("timeout_ms", C.c_uint)]
+                ("flags", C.c_void_p), ("timeout_ms", C.c_uint), ("gate_round", C.c_void_p),
+                ("gate_mult", C.c_uint)]
+
+
+class GhostEdge(C.Structure):
+    _fields_ = [("y_row", C.c_longlong), ("anchor_row", C.c_longlong), ("n", C.c_longlong),
+                ("u", C.c_void_p), ("p", C.c_void_p), ("du", C.c_void_p),
+                ("ready", C.c_void_p), ("epochs", C.c_void_p)]
+
+
+MAX_GHOST_EDGES = 16
+IPC_HANDLE_BYTES = 64
 
 
 class MseSet(C.Structure):
@@ -98,6 +109,12 @@ _SIGS = {
     "fr_nccl_destroy": [_P],
     "fr_exchange": [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(_P), C.POINTER(C.c_longlong), C.c_int,
                     C.POINTER(C.c_int), C.POINTER(_P), C.POINTER(C.c_longlong), C.c_int, _P],
+    "fr_ipc_alloc": [C.c_size_t, C.POINTER(_P), _P],
+    "fr_ipc_open": [_P, C.POINTER(_P)],
+    "fr_ipc_close": [_P],
+    "fr_ipc_free": [_P],
+    "fr_ghost_put": [_P, _P, _P, C.c_int, C.POINTER(GhostEdge), _P, C.c_uint, _P, _P],
+    "fr_counter_add": [_P, C.c_uint, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
@@ -145,7 +162,8 @@ def lib():
 LAUNCHERS = frozenset({
     "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_epoch_fwd_bwd_gated",
     "fr_signal", "fr_ghost_jet_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
-    "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_jet_act_forward",
+    "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_ghost_put", "fr_counter_add",
+    "fr_jet_act_forward",
     "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
 })
 launch_count = 0

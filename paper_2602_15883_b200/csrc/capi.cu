@@ -594,6 +594,8 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
     e.mse[i].lpart = lpart_blocks[1 + i];
     if (gate && gate->gate && i >= gate->first_gated_set) {
       e.mse[i].gate = gate->gate;
+      e.mse[i].gate_round = gate->gate_round;
+      e.mse[i].gate_mult = gate->gate_mult;
       e.mse[i].flags = gate->flags;
       e.mse[i].gate_timeout_ns = (unsigned long long)(gate->timeout_ms ? gate->timeout_ms : 60000u) * 1000000ull;
     }
@@ -919,6 +921,155 @@ extern "C" int fr_pack_ghost(const fr_plan* p, const void* y, const void* y_anch
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory ghost transport (see flowrec_b200.h).  One CTA per edge: thread 0
+// waits until the destination has finished the epoch that last read these
+// target rows, the block stores the rows straight into the destination's
+// memory (NVLink peer stores when it is another GPU), then thread 0 publishes
+// them with a system-scope release add on the destination's ready counter.
+// ---------------------------------------------------------------------------
+struct GhostEdges {
+  fr_ghost_edge e[FR_MAX_GHOST_EDGES];
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) ghost_put_kernel(const T* __restrict__ y, const T* __restrict__ yj,
+                                                        GhostEdges E, int nout, int nvel, int nin,
+                                                        const unsigned* my_epochs, unsigned long long timeout_ns,
+                                                        int* flags) {
+  const fr_ghost_edge& e = E.e[blockIdx.x];
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const unsigned need = *my_epochs;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int good = 1;
+    while (int(ld_acquire_sys(e.epochs) - need) < 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (flags) atomicOr(flags, FR_FLAG_EXCHANGE_TIMEOUT);
+        good = 0;
+        break;
+      }
+      __nanosleep(500);
+    }
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;  // the destination never freed its rows: leave them, the host raises DeadlockError
+  T* u = static_cast<T*>(e.u);
+  T* p = static_cast<T*>(e.p);
+  T* du = static_cast<T*>(e.du);
+  const T* yr = y + e.y_row * nout;
+  const T* ya = e.anchor_row >= 0 ? y + e.anchor_row * nout : nullptr;
+  for (long long i = threadIdx.x; i < e.n; i += blockDim.x) {
+    for (int c = 0; c < nvel; ++c) u[i * nvel + c] = yr[i * nout + c];
+    const T pv = yr[i * nout + nvel];
+    p[i] = ya ? pv - ya[i * nout + nvel] : pv;
+  }
+  if (du && yj) {
+    // jet rows (1 + 2 nin) x nout per point: first-derivative blocks 1..nin
+    const int S = 1 + 2 * nin;
+    const T* jr = yj + e.y_row * S * nout;
+    const long long tot = e.n * nin * nvel;
+    for (long long q = threadIdx.x; q < tot; q += blockDim.x) {
+      const long long i = q / (nin * nvel);
+      const int j = int(q / nvel % nin), c = int(q % nvel);
+      du[q] = jr[(i * S + 1 + j) * nout + c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(e.ready) : "memory");
+  }
+}
+
+__global__ void counter_add_kernel(unsigned* word, unsigned v) {
+  __threadfence_system();
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(word), "r"(v) : "memory");
+}
+
+extern "C" int fr_ipc_alloc(size_t bytes, void** ptr, void* handle_out) {
+  if (!ptr || !handle_out || bytes == 0) return fail("fr_ipc_alloc: bad arguments");
+  *ptr = nullptr;
+  void* d = nullptr;
+  FR_CUDA(cudaMalloc(&d, bytes), "fr_ipc_alloc");
+  cudaError_t e = cudaMemset(d, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, d);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(e, "fr_ipc_alloc");
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *ptr = d;
+  return 0;
+}
+
+extern "C" int fr_ipc_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return fail("fr_ipc_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  FR_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "fr_ipc_open");
+  return 0;
+}
+
+extern "C" int fr_ipc_close(void* ptr) {
+  if (!ptr) return 0;
+  FR_CUDA(cudaIpcCloseMemHandle(ptr), "fr_ipc_close");
+  return 0;
+}
+
+extern "C" int fr_ipc_free(void* ptr) {
+  if (!ptr) return 0;
+  FR_CUDA(cudaFree(ptr), "fr_ipc_free");
+  return 0;
+}
+
+extern "C" int fr_ghost_put(const fr_plan* p, const void* y, const void* y_jet, int n_edges, const fr_ghost_edge* edges,
+                            const unsigned* my_epochs, unsigned timeout_ms, int* flags, fr_stream_t stream) {
+  if (!p || !edges || !my_epochs || n_edges < 0 || n_edges > FR_MAX_GHOST_EDGES)
+    return fail("fr_ghost_put: bad arguments");
+  if (n_edges == 0) return 0;
+  if (!y) return fail("fr_ghost_put: NULL producer output");
+  GhostEdges E{};
+  for (int i = 0; i < n_edges; ++i) {
+    const fr_ghost_edge& e = edges[i];
+    if (e.n < 0 || (e.n > 0 && (!e.u || !e.p)) || !e.ready || !e.epochs || e.y_row < 0)
+      return fail("fr_ghost_put: bad edge %d", i);
+    if (e.du && !y_jet) return fail("fr_ghost_put: edge %d carries derivatives but y_jet is NULL", i);
+    E.e[i] = e;
+  }
+  const fr_plan_info& I = p->info;
+  const unsigned long long tns = (unsigned long long)(timeout_ms ? timeout_ms : 600000u) * 1000000ull;
+  if (I.dtype == FR_F32)
+    ghost_put_kernel<float><<<n_edges, 256, 0, stream>>>(static_cast<const float*>(y), static_cast<const float*>(y_jet),
+                                                          E, I.n_out, I.n_vel, I.n_in, my_epochs, tns, flags);
+  else
+    ghost_put_kernel<double><<<n_edges, 256, 0, stream>>>(static_cast<const double*>(y),
+                                                           static_cast<const double*>(y_jet), E, I.n_out, I.n_vel,
+                                                           I.n_in, my_epochs, tns, flags);
+  ++g_kernel_launches;
+  FR_CUDA(cudaGetLastError(), "fr_ghost_put");
+  return 0;
+}
+
+extern "C" int fr_counter_add(unsigned* word, unsigned value, fr_stream_t stream) {
+  if (!word) return fail("fr_counter_add: NULL word");
+  counter_add_kernel<<<1, 1, 0, stream>>>(word, value);
+  ++g_kernel_launches;
+  FR_CUDA(cudaGetLastError(), "fr_counter_add");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
 // Reference seam (_kernels): elementwise jet propagation on stacked f64 arrays
 // ((1 + 2d) * batch, width).  Semantics of numpy_backend.py:43-89, including
 // "written" (accumulate=0) versus "added" adjoints.
@@ -1047,5 +1198,8 @@ static int preload_capi_kernels() {
   FR_CUDA(cudaFuncGetAttributes(&fa, pack_ghost_kernel<double>), "preload fr_pack_ghost");
   FR_CUDA(cudaFuncGetAttributes(&fa, prepare_kernel<float>), "preload fr_prepare_params");
   FR_CUDA(cudaFuncGetAttributes(&fa, prepare_kernel<double>), "preload fr_prepare_params");
+  FR_CUDA(cudaFuncGetAttributes(&fa, ghost_put_kernel<float>), "preload fr_ghost_put");
+  FR_CUDA(cudaFuncGetAttributes(&fa, ghost_put_kernel<double>), "preload fr_ghost_put");
+  FR_CUDA(cudaFuncGetAttributes(&fa, counter_add_kernel), "preload fr_counter_add");
   return 0;
 }

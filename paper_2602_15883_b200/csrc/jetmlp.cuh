@@ -89,7 +89,9 @@ struct KArgs {
   double inv_re;        // PDE: 1/Re (physics.py:80)
   double velw[4];       // MSE: velocity component weights
   int has_p;            // MSE: pressure head present
-  const unsigned* gate; // MSE: wait until *gate != 0 before the first tile (ghost overlap)
+  const unsigned* gate; // MSE: wait before the first tile (ghost overlap) until *gate != 0, or,
+  const unsigned* gate_round;  // when non-null, until *gate >= *gate_round * gate_mult
+  unsigned gate_mult;          //   (monotonic arrival counter of the peer-memory transport)
   int* flags;           // FLAG_EXCHANGE_TIMEOUT on a timed-out gate wait
   unsigned long long gate_timeout_ns;
 };

@@ -192,13 +192,17 @@ struct JetCfg {
 // Ghost-overlap gate (fr_epoch_gate): spin with back-off until the transport
 // stream has published this rank's ghost targets; bounded, so a lost peer
 // becomes a flagged error instead of a hung GPU.
-static __device__ __noinline__ void gate_wait(const unsigned* gate, int* flags, unsigned long long timeout_ns) {
+// With `round` the gate is a monotonic arrival counter written by peers over
+// NVLink (fr_ghost_put): wait until it reaches *round * mult (system scope).
+static __device__ __noinline__ void gate_wait(const unsigned* gate, const unsigned* round, unsigned mult, int* flags,
+                                              unsigned long long timeout_ns) {
   unsigned long long t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const unsigned target = round ? *round * mult : 1u;
   for (;;) {
     unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
-    if (v != 0u) return;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+    if (int(v - target) >= 0) return;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > timeout_ns) {
       if (flags) atomicOr(flags, FLAG_EXCHANGE_TIMEOUT);
@@ -547,7 +551,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   const long long ntiles = (n + PPT - 1) / PPT;
   if constexpr (MODE == MODE_MSE) {
     if (a.gate != nullptr && t0 < ntiles) {
-      if (tid == 0) gate_wait(a.gate, a.flags, a.gate_timeout_ns);
+      if (tid == 0) gate_wait(a.gate, a.gate_round, a.gate_mult, a.flags, a.gate_timeout_ns);
       __syncthreads();
     }
   }

@@ -137,17 +137,45 @@ class LocalTrainer:
     the in-kernel wait, not stream order, protects the ghost heads)."""
 
     def __init__(self, plan: TrainingPlan, dtype="float32", epochs=None, overlap=False, reserve_sms=None,
-                 signal_delay_ns=0, exchange_timeout=600.0):
+                 signal_delay_ns=0, exchange_timeout=600.0, transport="device"):
+        """transport="device": packs write the destinations' target rows in
+        stream order (or on a side stream with overlap=True); "peer": every
+        rank runs the peer-memory protocol of the one-process-per-GPU trainer
+        (runtime/peer.py: fr_ghost_put into the destination's IPC block, the
+        ready / epochs counters, the counter-gated epoch kernel), enqueued on
+        one stream so each wait is already satisfied when it is reached."""
+        if transport not in ("device", "peer"):
+            raise ValueError(f"unknown transport {transport!r} (use 'device' or 'peer')")
+        if transport == "peer" and overlap:
+            raise ValueError("the in-process peer transport runs stream-ordered (overlap=False)")
         self.plan = plan
+        self.transport = transport
         self.exchange_timeout = float(exchange_timeout)
         self.overlap = bool(overlap)
         self.signal_delay_ns = int(signal_delay_ns)
         if reserve_sms is None:
             reserve_sms = 2 if self.overlap else 0
         max_ctas = _overlap_max_ctas(reserve_sms) if reserve_sms else 0
-        self.workers = {ws.rank: RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas)
+        self.blocks = {}
+        if transport == "peer":
+            from .peer import IpcBlock
+
+            dev = torch.device("cuda", torch.cuda.current_device())
+            tdt = torch.float32 if dtype in ("float32", "f32") else torch.float64
+            self.blocks = {ws.rank: IpcBlock(ws, tdt, dev, plan.train_config.ghost_derivative_weight > 0)
+                           for ws in plan.worker_specs}
+        self.workers = {ws.rank: RankWorker(ws, dtype=dtype, epochs=epochs, max_ctas=max_ctas,
+                                            target_alloc=self.blocks[ws.rank].alloc if self.blocks else None)
                         for ws in plan.worker_specs}
         self.order = sorted(self.workers)
+        if transport == "peer":
+            from .peer import PeerRank
+
+            self.peers = {r: PeerRank(self.workers[r], self.blocks[r], self.exchange_timeout) for r in self.order}
+            info = {r: (self.blocks[r].ptr, self.blocks[r].target_offsets(self.workers[r].objective))
+                    for r in self.order}
+            for r in self.order:
+                self.peers[r].connect(info)
         if self.overlap:
             self.comm = torch.cuda.Stream()
             self.gates = torch.zeros(len(self.order), dtype=torch.int32, device="cuda")
@@ -177,6 +205,13 @@ class LocalTrainer:
             self.workers[r].enqueue_epoch()
 
     def _enqueue(self, exchange):
+        if self.transport == "peer":
+            if exchange:
+                for r in self.order:
+                    self.peers[r].put()
+            for r in self.order:
+                self.peers[r].step(exchange)
+            return
         if exchange and self.overlap:
             self._enqueue_overlapped()
             return
@@ -350,8 +385,17 @@ class FrNcclTransport:
 
 
 class DistributedTrainer:
-    """This process's rank of a torch.distributed group (NCCL over NVLink).
+    """This process's rank of a torch.distributed group (one process per GPU).
 
+    transport="ipc" (default): the peer-memory exchange of runtime/peer.py --
+    the producer's put kernel stores the ghost rows straight into the
+    neighbours' target blocks over NVLink (CUDA IPC mappings), arrivals are
+    counted in the receiver's `ready` word and its epoch kernel's ghost sets
+    wait on that count in-kernel; no NCCL call and no host synchronisation
+    per epoch, so every epoch after the first is ONE CUDA graph replay.
+    torch.distributed is used once, to exchange the IPC handles.
+
+    transport="torch" / "fr_nccl" (NCCL point-to-point, enqueued eagerly):
     overlap=True (default for the fused small-width kernel): the ghost
     transfer is overlapped with the interior work.  The producer (value
     forward of the neighbours' ghost points) and the pack run on the compute
@@ -368,17 +412,24 @@ class DistributedTrainer:
     synchronise the device)."""
 
     def __init__(self, plan: TrainingPlan, rank=None, dtype="float32", epochs=None, overlap=True, reserve_sms=None,
-                 transport="torch", exchange_timeout=600.0):
+                 transport="ipc", exchange_timeout=600.0):
         import torch.distributed as dist
 
-        if transport not in ("torch", "fr_nccl"):
-            raise ValueError(f"unknown transport {transport!r} (use 'torch' or 'fr_nccl')")
+        if transport not in ("torch", "fr_nccl", "ipc"):
+            raise ValueError(f"unknown transport {transport!r} (use 'ipc', 'torch' or 'fr_nccl')")
 
         self.plan = plan
+        self.transport = transport
         self.rank = dist.get_rank() if rank is None else rank
         if dist.get_world_size() != plan.n_ranks:
             raise ValueError(f"world size {dist.get_world_size()} != plan ranks {plan.n_ranks}")
         ws = plan.worker_specs[self.rank]
+        self.graphs = {}
+        self.launches_per_epoch = {}  # library kernels in each captured epoch graph
+        self._ran_eager = False
+        if transport == "ipc":
+            self._init_ipc(plan, ws, dtype, epochs, exchange_timeout)
+            return
         wide = max(plan.expert_config.arch[1:-1], default=0) > 64
         self.overlap = bool(overlap) and not wide and len(ws.datasets.ghosts) > 0
         max_ctas = 0
@@ -410,14 +461,83 @@ class DistributedTrainer:
             # (driver.py:150-181): a lost peer -> FLAG_EXCHANGE_TIMEOUT -> DeadlockError
             self.gate = w.objective.make_gate(self.gate_word, w.flags, exchange_timeout)
 
+    def _init_ipc(self, plan, ws, dtype, epochs, exchange_timeout):
+        """Peer-memory transport (runtime/peer.py): the neighbours' target
+        blocks are mapped into this process (CUDA IPC, peer access over
+        NVLink); every epoch is a fixed kernel sequence, replayed from CUDA
+        graphs after the first."""
+        import torch.distributed as dist
+
+        from .peer import IpcBlock, PeerRank, open_peer
+
+        self.overlap = False
+        dev = torch.device("cuda", torch.cuda.current_device())
+        tdt = torch.float32 if dtype in ("float32", "f32") else torch.float64
+        self.block = IpcBlock(ws, tdt, dev, plan.train_config.ghost_derivative_weight > 0)
+        self.worker = w = RankWorker(ws, dtype=dtype, epochs=epochs, target_alloc=self.block.alloc)
+        torch.cuda.synchronize()  # the block is zeroed before any peer can store into it
+        mine = (self.rank, self.block.handle, self.block.target_offsets(w.objective))
+        table = [None] * plan.n_ranks
+        dist.all_gather_object(table, mine)
+        self.peer_ptrs = {}
+        info = {}
+        for r, handle, offsets in table:
+            if r in {e.dest for e in ws.outgoing}:
+                self.peer_ptrs[r] = open_peer(handle)
+                info[r] = (self.peer_ptrs[r], offsets)
+        self.peer = PeerRank(w, self.block, exchange_timeout)
+        self.peer.connect(info)
+
+    def _enqueue_ipc(self, exchange):
+        if exchange:
+            self.peer.put()
+        self.peer.step(exchange)
+
+    def _ipc_epoch(self, exchange, use_graphs=True):
+        if use_graphs and self._ran_eager:
+            w = self.worker
+            if w.epochs_done + 1 > w.capacity:
+                raise RuntimeError("history capacity exhausted; construct the trainer with more epochs")
+            g = self.graphs.get(exchange)
+            if g is None:
+                from .. import _lib as X
+
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                k0 = X.kernel_launches()
+                with torch.cuda.graph(g):
+                    self._enqueue_ipc(exchange)
+                self.launches_per_epoch[exchange] = X.kernel_launches() - k0
+                self.graphs[exchange] = g
+            g.replay()
+        else:
+            self._enqueue_ipc(exchange)
+            self._ran_eager = True
+
+    def close(self):
+        """Unmap the peers' blocks (IPC) / destroy the library's communicator."""
+        from .. import _lib as X
+
+        for ptr in getattr(self, "peer_ptrs", {}).values():
+            X.call("fr_ipc_close", C.c_void_p(ptr))
+        self.peer_ptrs = {}
+        if getattr(self, "_post", None) is not None and hasattr(self._post, "close"):
+            self._post.close()
+
     def _du(self, k):
         b = self.send_bufs[k]
         return b[2] if len(b) > 2 else None
 
-    def epoch(self, e):
+    def epoch(self, e, use_graphs=True):
         """Exchange (if due) then the fused epoch (overlapped, see the class doc)."""
         w = self.worker
         exchange = e % self.plan.train_config.comm_interval == 0
+        if self.transport == "ipc":
+            self._ipc_epoch(exchange, use_graphs)
+            w.epochs_done += 1
+            if exchange:
+                w.exchange_log.append((e, sorted(w.expected_messages)))
+            return
         cur = torch.cuda.current_stream()
         if exchange and self.overlap and self._connected:
             # producer + pack on the compute stream (~20 us on the full GPU);
@@ -468,14 +588,16 @@ class DistributedTrainer:
         return times
 
 
-def _train_distributed(plan, dtype, exchange_timeout=600.0):
+def _train_distributed(plan, dtype, exchange_timeout=600.0, transport="ipc"):
     import torch.distributed as dist
 
     t0 = time.perf_counter()
-    tr = DistributedTrainer(plan, dtype=dtype, exchange_timeout=exchange_timeout)
+    tr = DistributedTrainer(plan, dtype=dtype, exchange_timeout=exchange_timeout, transport=transport)
     tr.run(plan.train_config.epochs)
     exports = [None] * plan.n_ranks
     dist.all_gather_object(exports, (tr.rank, tr.worker.export()))
+    dist.barrier()  # no peer may unmap / free a block another rank still stores into
+    tr.close()
     return _collect(plan, dict(exports), time.perf_counter() - t0)
 
 

@@ -41,8 +41,16 @@ def check_finite(name, arr):
 class DeviceObjective:
     """Resident datasets, workspaces and the per-epoch launch sequence."""
 
-    def __init__(self, plan, regime, datasets, weights, max_ctas=0, ghost_derivative_weight=0.0):
+    def __init__(self, plan, regime, datasets, weights, max_ctas=0, ghost_derivative_weight=0.0,
+                 target_alloc=None):
+        """target_alloc(kind, name, shape) -> zeroed device tensor: where the
+        ghost-target rows live (default: torch allocations; the peer-memory
+        transport passes views of its IPC block so neighbours can store into
+        them directly)."""
         self.plan = plan
+        if target_alloc is None:
+            target_alloc = lambda kind, name, shape: torch.zeros(shape, dtype=plan.tdtype, device=plan.device)  # noqa: E731
+        self.target_alloc = target_alloc
         self.max_ctas = int(max_ctas)  # persistent-grid cap (SMs left free for the exchange transport)
         # opt-in C^1 interface extension (0: the reference's value-only coupling)
         self.gd_weight = float(ghost_derivative_weight)
@@ -94,8 +102,8 @@ class DeviceObjective:
             p_w = weights.ghost_p_space if kind == "spatial" else weights.ghost_p_time
             self.ghost[kind] = {
                 "pts": to_device(np.vstack(per_kind[kind]), T, dev),
-                "tu": torch.zeros((counts[kind], nv), dtype=T, device=dev),
-                "tp": torch.zeros(counts[kind], dtype=T, device=dev),
+                "tu": target_alloc(kind, "tu", (counts[kind], nv)),
+                "tp": target_alloc(kind, "tp", (counts[kind],)),
                 "vel_coef": weights.ghost_u / self.n_ghost_total,
                 "p_coef": p_w / counts[kind],
             }
@@ -162,7 +170,7 @@ class DeviceObjective:
             lrow = 0
             for kind, g in self.ghost.items():
                 n = g["pts"].shape[0]
-                g["tdu"] = torch.zeros((n, n_in, nv), dtype=plan.tdtype, device=dev)
+                g["tdu"] = self.target_alloc(kind, "tdu", (n, n_in, nv))
                 ws = plan.workspace(X.MODE_GJ, n)
                 self.gd_launches.append((kind, n, rows, lrow, ws))
                 rows += ws.grid
