@@ -89,3 +89,79 @@ def test_peer_put_times_out_when_destination_never_frees(golden):
     torch.cuda.synchronize()
     with pytest.raises(DeadlockError):
         tr.workers[0].check_flags()
+
+
+def _ipc_child(handle, q):
+    try:
+        import ctypes as C
+
+        import torch
+
+        from paper_2602_15883_b200 import _lib as X
+        from paper_2602_15883_b200.runtime.peer import READY, open_peer
+
+        torch.cuda.set_device(0)
+        base = open_peer(handle)
+        X.call("fr_counter_add", C.c_void_p(base + READY), 7, X.stream_ptr())
+        torch.cuda.synchronize()
+        X.call("fr_ipc_close", C.c_void_p(base))
+        q.put("ok")
+    except Exception:
+        import traceback
+
+        q.put(traceback.format_exc())
+
+
+def test_ipc_handle_opens_in_another_process():
+    """The block a DistributedTrainer publishes is writable from another
+    process through its IPC handle (no kernel waits on another here: the child
+    adds to the parent's ready word and exits, then the parent reads it)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2602_15883_b200.runtime.peer import IpcBlock
+
+    _, plan = training_plan("t2", __import__("numpy").load(__import__("conftest").GOLDEN))
+    blk = IpcBlock(plan.worker_specs[0], torch.float32, torch.device("cuda", 0))
+    torch.cuda.synchronize()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ipc_child, args=(blk.handle, q))
+    p.start()
+    msg = q.get(timeout=300)
+    p.join(timeout=60)
+    assert msg == "ok", msg
+    assert int(blk.ready.item()) == 7
+    blk.free()
+
+
+def test_distributed_trainer_ipc_world1(golden):
+    """DistributedTrainer(transport='ipc') end to end in a one-rank group
+    (handle table over torch.distributed, graph replays) == LocalTrainer."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2602_15883_b200.runtime.driver import DistributedTrainer, LocalTrainer
+
+    _, plan = training_plan("p1", golden)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        tr = DistributedTrainer(plan, transport="ipc")
+        tr.run(plan.train_config.epochs)
+        assert set(tr.graphs) == {True} and tr.launches_per_epoch[True] > 0
+        ref = LocalTrainer(plan)
+        ref.run(plan.train_config.epochs)
+        assert np.array_equal(tr.worker.flat.cpu().numpy(), ref.workers[0].flat.cpu().numpy())
+        tr.worker.sync_history()
+        ref.workers[0].sync_history()
+        assert np.array_equal(np.array(tr.worker.history)[:, 1:], np.array(ref.workers[0].history)[:, 1:])
+        tr.close()
+    finally:
+        dist.destroy_process_group()
