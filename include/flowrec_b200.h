@@ -221,6 +221,15 @@ int fr_ghost_put(const fr_plan* plan, const void* y, const void* y_jet, int n_ed
 /* *word += value (release, system scope) once prior work on `stream` is done */
 int fr_counter_add(unsigned* word, unsigned value, fr_stream_t stream);
 
+/* GPU-side dataset sampling: out[i][j] (row-major n x n_cols,
+ * f64 and/or f32) = the value NumPy's Generator(PCG64) produces for
+ * rng.uniform(lo[j], hi[j], size=n) called once per column j in order
+ * (decomposition.py:64-70), starting `skip` draws into the stream whose state
+ * before the first draw is state4 = {state >> 64, state & (2^64-1), inc >> 64,
+ * inc & (2^64-1)} (e.g. PCG64(SeedSequence([seed, rank, tag])).state).  Bit-exact. */
+int fr_pcg64_uniform(const unsigned long long* state4, unsigned long long skip, long long n, int n_cols,
+                     const double* lo, const double* hi, double* out64, float* out32, fr_stream_t stream);
+
 /* value forward: out (n, n_out) */
 int fr_value_fwd(const fr_plan* plan, const void* kparams, const void* pts, long long n, void* out,
                  fr_stream_t stream);

@@ -115,6 +115,8 @@ _SIGS = {
     "fr_ipc_free": [_P],
     "fr_ghost_put": [_P, _P, _P, C.c_int, C.POINTER(GhostEdge), _P, C.c_uint, _P, _P],
     "fr_counter_add": [_P, C.c_uint, _P],
+    "fr_pcg64_uniform": [C.POINTER(C.c_ulonglong), C.c_ulonglong, C.c_longlong, C.c_int, C.POINTER(C.c_double),
+                         C.POINTER(C.c_double), _P, _P, _P],
     "fr_value_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_jet_fwd": [_P, _P, _P, C.c_longlong, _P, _P],
     "fr_reduce_grad": [_P, _P, C.c_int, _P, C.c_int, _P, _P],
@@ -163,6 +165,7 @@ LAUNCHERS = frozenset({
     "fr_prepare_params", "fr_pde_fwd_bwd", "fr_mse_fwd_bwd", "fr_epoch_fwd_bwd", "fr_epoch_fwd_bwd_gated",
     "fr_signal", "fr_ghost_jet_fwd_bwd", "fr_value_fwd", "fr_jet_fwd",
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_ghost_put", "fr_counter_add",
+    "fr_pcg64_uniform",
     "fr_jet_act_forward",
     "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
 })

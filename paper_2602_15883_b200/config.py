@@ -50,17 +50,18 @@ class Problem:
 
 def cylinder2d_problem(n_procs=1, n_pde=500_000, n_ghost=1000, per_snapshot=200, grid_nx=33,
                        snapshots=50, hidden_layers=4, width=64, activation="tanh", seed=0,
-                       counts=None, time_splits=None):
+                       counts=None, time_splits=None, colloc_on_device=False):
     """2D cylinder-wake-shaped config: Taylor-Green at Re=100
     on [-7.5, 17.5] x [-8, 8], t in [0, 7.35], 50 snapshots, delta 2.0 / 1.0."""
     sol = benchmarks.TaylorGreen2D(re=100.0, spatial_box=((-7.5, 17.5), (-8.0, 8.0)), time_interval=(0.0, 7.35))
     return _assemble(sol, n_procs, n_pde, n_ghost, per_snapshot, grid_nx, snapshots, hidden_layers, width,
-                     activation, seed, (2.0, 1.0), LossWeights(10.0, 5.0, 1.0, 1.0, 1.0), counts, time_splits)
+                     activation, seed, (2.0, 1.0), LossWeights(10.0, 5.0, 1.0, 1.0, 1.0), counts, time_splits,
+                     colloc_on_device)
 
 
 def cylinder3d_problem(n_procs=8, n_pde=600_000, n_ghost=5000, per_snapshot=1250, grid_nx=17,
                        snapshots=80, hidden_layers=8, width=64, activation="sin", seed=0,
-                       counts=None, time_splits=None):
+                       counts=None, time_splits=None, colloc_on_device=False):
     """3D wake-shaped config: Beltrami at Re=300 on
     [-5, 20] x [-5, 5] x [0, 10], t in [0, 11.85]; weights (10, 10, 1, 1),
     velocity weights (1, 5, 100)."""
@@ -68,11 +69,11 @@ def cylinder3d_problem(n_procs=8, n_pde=600_000, n_ghost=5000, per_snapshot=1250
                                 time_interval=(0.0, 11.85))
     w = LossWeights(10.0, 10.0, 1.0, 1.0, 1.0, velocity=(1.0, 5.0, 100.0))
     return _assemble(sol, n_procs, n_pde, n_ghost, per_snapshot, grid_nx, snapshots, hidden_layers, width,
-                     activation, seed, (2.0, 2.0), w, counts, time_splits)
+                     activation, seed, (2.0, 2.0), w, counts, time_splits, colloc_on_device)
 
 
 def _assemble(sol, n_procs, n_pde, n_ghost, per_snapshot, grid_nx, snapshots, hidden_layers, width,
-              activation, seed, deltas, weights, counts, time_splits):
+              activation, seed, deltas, weights, counts, time_splits, colloc_on_device=False):
     regime = sol.regime
     domain = GlobalDomain.from_solution(sol)
     if counts is None:
@@ -83,7 +84,7 @@ def _assemble(sol, n_procs, n_pde, n_ghost, per_snapshot, grid_nx, snapshots, hi
     obs = snapshot_observations(table, per_snapshot, seed=0)
     budget = Budget(n_obs=obs.n, n_pde=n_pde, n_ghost_per_interface=n_ghost)
     subs = partition(domain, counts, time_splits, delta_space=deltas[0], delta_time=deltas[1])
-    datasets = build_all_rank_datasets(subs, budget, obs, seed)
+    datasets = build_all_rank_datasets(subs, budget, obs, seed, colloc_on_device=colloc_on_device)
     cfg = ExpertConfig.for_regime(regime, hidden_layers, width, activation)
     anchor = tuple(lo + 0.25 * (hi - lo) for lo, hi in domain.spatial_box)
     return Problem(sol, domain, subs, datasets, cfg, weights, anchor, budget, table)

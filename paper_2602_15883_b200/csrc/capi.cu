@@ -1070,6 +1070,91 @@ extern "C" int fr_counter_add(unsigned* word, unsigned value, fr_stream_t stream
 }
 
 // ---------------------------------------------------------------------------
+// GPU-side dataset sampling, bit-exact with NumPy's Generator(PCG64).uniform
+// (decomposition.py:64-70: one rng.uniform(lo, hi, size=n) per column, columns
+// in layout order).  PCG64 = 128-bit LCG, XSL-RR 128/64 output of the stepped
+// state; next_double = (x >> 11) * 2^-53; uniform = lo + (hi - lo) * u with
+// round-to-nearest f64 ops (no contraction), as NumPy's random_uniform.  Draw d
+// of the stream (d = skip + column * n + row) is reached by LCG jump-ahead, so
+// every thread produces its own contiguous run of draws.
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+struct UniformCols {
+  double lo[8], range[8];
+};
+
+__device__ __forceinline__ u128 pcg_mult() {
+  return (u128(0x2360ED051FC65DA4ull) << 64) | u128(0x4385DF649FCCF645ull);
+}
+
+__device__ __forceinline__ u128 pcg_advance(u128 state, u128 inc, unsigned long long delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta > 0) {
+    if (delta & 1ull) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+__device__ __forceinline__ unsigned long long pcg_output(u128 s) {
+  const unsigned long long x = (unsigned long long)(s >> 64) ^ (unsigned long long)s;
+  const unsigned rot = unsigned(s >> 122);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+__global__ void __launch_bounds__(256) pcg64_uniform_kernel(unsigned long long s_hi, unsigned long long s_lo,
+                                                            unsigned long long i_hi, unsigned long long i_lo,
+                                                            unsigned long long skip, long long n, int ncols,
+                                                            UniformCols cols, long long per_thread, double* out64,
+                                                            float* out32) {
+  const long long total = n * ncols;
+  const long long d0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * per_thread;
+  if (d0 >= total) return;
+  const u128 inc = (u128(i_hi) << 64) | u128(i_lo);
+  // state before draw d0: advanced skip + d0 steps; each draw steps first
+  u128 st = pcg_advance((u128(s_hi) << 64) | u128(s_lo), inc, skip + (unsigned long long)d0);
+  const u128 mult = pcg_mult();
+  const long long d1 = d0 + per_thread < total ? d0 + per_thread : total;
+  for (long long d = d0; d < d1; ++d) {
+    st = st * mult + inc;
+    const double u = double(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+    const int j = int(d / n);
+    const long long i = d - (long long)j * n;
+    const double v = __dadd_rn(cols.lo[j], __dmul_rn(cols.range[j], u));
+    if (out64) out64[i * ncols + j] = v;
+    if (out32) out32[i * ncols + j] = float(v);
+  }
+}
+
+extern "C" int fr_pcg64_uniform(const unsigned long long* state4, unsigned long long skip, long long n, int n_cols,
+                                const double* lo, const double* hi, double* out64, float* out32,
+                                fr_stream_t stream) {
+  if (!state4 || !lo || !hi || n < 0 || n_cols < 1 || n_cols > 8 || (!out64 && !out32))
+    return fail("fr_pcg64_uniform: bad arguments");
+  if (n == 0) return 0;
+  UniformCols c{};
+  for (int j = 0; j < n_cols; ++j) {
+    c.lo[j] = lo[j];
+    c.range[j] = hi[j] - lo[j];  // NumPy: _range = high - low (a Python float subtraction)
+    if (!std::isfinite(c.range[j])) return fail("fr_pcg64_uniform: non-finite range in column %d", j);
+  }
+  const long long total = n * n_cols;
+  const long long per_thread = 64;  // sequential steps per thread after one jump-ahead
+  const long long threads = (total + per_thread - 1) / per_thread;
+  const int blocks = int((threads + 255) / 256);
+  pcg64_uniform_kernel<<<blocks, 256, 0, stream>>>(state4[0], state4[1], state4[2], state4[3], skip, n, n_cols, c,
+                                                   per_thread, out64, out32);
+  ++g_kernel_launches;
+  FR_CUDA(cudaGetLastError(), "fr_pcg64_uniform");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
 // Reference seam (_kernels): elementwise jet propagation on stacked f64 arrays
 // ((1 + 2d) * batch, width).  Semantics of numpy_backend.py:43-89, including
 // "written" (accumulate=0) versus "added" adjoints.

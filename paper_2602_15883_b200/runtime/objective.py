@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 from .. import _lib as X
+from ..decomposition import DeviceUniform
 from ..engine import get_plan, new_kparams, prepare, to_device
 from ..physics import LossParts, compose_loss
 
@@ -74,7 +75,9 @@ class DeviceObjective:
 
         # the reference validates every input it binds (tape.py:298-313); the
         # datasets are resident here, so they are checked once
-        check_finite("input 'points'", datasets.colloc_points)
+        device_colloc = isinstance(datasets.colloc_points, DeviceUniform)  # sampled on the GPU
+        if not device_colloc:
+            check_finite("input 'points'", datasets.colloc_points)  # (a device sample is finite by construction)
         if self.n_obs:
             check_finite("input 'points'", datasets.obs_points)
             check_finite("input 'target_u'", datasets.obs_velocity)
@@ -82,7 +85,8 @@ class DeviceObjective:
             check_finite("input 'points'", g.points)
         self.obs_pts = to_device(datasets.obs_points.reshape(-1, regime.n_inputs), T, dev)
         self.obs_vel = to_device(datasets.obs_velocity.reshape(-1, nv), T, dev)
-        self.col_pts = to_device(datasets.colloc_points, T, dev)
+        self.col_pts = (datasets.colloc_points.to_device("float32" if T == torch.float32 else "float64", dev)
+                        if device_colloc else to_device(datasets.colloc_points, T, dev))
 
         # ghost sets grouped per kind in ghost-index order (objective.py:115-141)
         self.ghost_slices = {}  # ghost index -> (kind, offset, n)

@@ -201,3 +201,20 @@ def test_headline_inputs_bit_exact_with_reference():
         assert np.array_equal(d.obs_points, hg[f"ep/{r}/obs_points"])
         for gi, g in enumerate(d.ghosts):
             assert np.array_equal(g.points, hg[f"ep/{r}/ghost{gi}"])
+
+
+def test_device_uniform_host_view_is_the_reference_sample():
+    """DeviceUniform (GPU sampling stand-in) keeps the host contract: its NumPy
+    view equals the reference's sample_uniform draw bit for bit, and its shape
+    is known without sampling."""
+    from paper_2602_15883_b200 import config as fconfig
+
+    host = fconfig.cylinder2d_problem(n_pde=20_000, counts=(2, 2), time_splits=2)
+    lazy = fconfig.cylinder2d_problem(n_pde=20_000, counts=(2, 2), time_splits=2, colloc_on_device=True)
+    for r in range(8):
+        d = lazy.datasets[r].colloc_points
+        assert d.shape == host.datasets[r].colloc_points.shape and d._host is None
+        assert lazy.datasets[r].n_colloc == host.datasets[r].n_colloc
+        assert np.array_equal(np.asarray(d), host.datasets[r].colloc_points)
+        for ga, gb in zip(lazy.datasets[r].ghosts, host.datasets[r].ghosts):
+            assert np.array_equal(ga.points, gb.points)  # ghosts: their own stream (tag 2)
