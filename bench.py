@@ -230,7 +230,7 @@ def run_ours(args):
         pb = cylinder3d_problem(n_procs=n_sub, n_pde=args.n_pde, **arch)
     total_epochs = args.warmup + args.steps + args.e2e_steps + 2
     tc = TrainConfig(epochs=total_epochs, batch_size=25000, learning_rate=1e-3, weights=pb.weights,
-                     anchor=pb.anchor, lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0)
+                     anchor=pb.anchor, lr_factor=0.2, lr_interval=2000, comm_interval=1, seed=0, math=args.math)
     plan = build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc)
     if world == 1:
         trainer = LocalTrainer(plan, dtype=args.dtype, epochs=total_epochs)
@@ -351,7 +351,9 @@ def run_ours(args):
     # ---- dominant kernel: the fused PDE jet-MLP fwd+bwd, timed alone ----
     pde = _time_epoch_kernel(torch, X, worker) if not worker.objective.wide else _time_wide_pde(torch, X, worker)
     tf32 = worker.plan.info.math == 1 and worker.objective.wide
+    tc3 = worker.plan.info.math == 2 and not worker.objective.wide  # split-TF32 epoch kernel (W <= 64)
     peak = (measure_tf32_peak(torch) if tf32 else measure_fp32_peak(torch, X)) if rank == 0 else None
+    tf32_peak = measure_tf32_peak(torch) if (rank == 0 and tc3) else None
     if dist is not None:
         dist.barrier()
 
@@ -409,8 +411,11 @@ def run_ours(args):
             "launches_per_step": lp,
             "roofline": {
                 "bound": "tensor" if tf32 else "compute",
-                "pipe": "tf32 tcgen05.mma (TMEM accumulators)" if tf32 else "fp32-simt (FFMA)",
-                "kernel": ("jetmlp_epoch_kernel<float,tanh,unsteady2d,64> (fr_epoch_fwd_bwd: PDE + obs/ghost heads)"
+                "pipe": ("tf32 tcgen05.mma (TMEM accumulators)" if tf32 else
+                         "tcgen05 split-TF32 (forward + adjoint contractions) + FP32 SIMT (jets, dW); FP32-equivalent "
+                         "algorithmic flops over the FP32 SIMT peak" if tc3 else "fp32-simt (FFMA)"),
+                "kernel": ("jetmlp_epoch_kernel<float,tanh,unsteady2d,64" + (",TC>" if tc3 else ">")
+                           + " (fr_epoch_fwd_bwd: PDE + obs/ghost heads)"
                            if not obj.wide else
                            "TF32 tcgen05 layer-wise kernels (fr_pde_fwd_bwd, PDE set only: tcw_fwd/head/dx/dw)"
                            if tf32 else "SIMT layer-wise wide kernels (fr_pde_fwd_bwd, PDE set only)"),
@@ -424,6 +429,7 @@ def run_ours(args):
                 "traffic": _traffic(args.config, n_sub, world),
             },
             **({"hbm_design": hbm} if hbm else {}),
+            **({"tensor_pipe": _tc3_tensor(pde, obj, L, W, tf32_peak)} if tc3 else {}),
             "clocks": clk,
             "host_launches_timed": launches_host,
             "host_enqueue_ms_per_step": host_s / args.steps * 1e3,
@@ -456,6 +462,25 @@ def _extra_config(config_id, args):
     keep = ("value", "unit", "ms_per_step", "iters_per_s", "steps", "warmup", "dtype", "config", "e2e",
             "gpu_launches", "roofline", "clocks")
     return {k: d[k] for k in keep if k in d}
+
+
+def _tc3_tensor(pde, obj, L, W, tf32_peak):
+    """Tensor-pipe view of the split-TF32 epoch kernel: per tile and hidden
+    layer, the forward and the adjoint contraction each run one N = 2W MMA
+    (trunc(A) [B_hi | B_lo]) and one N = W MMA (A_lo B_hi) over the tile's
+    128-row blocks."""
+    ws = obj.ws
+    nt = ws.threads
+    rows = (nt // (W // 8)) * 6  # 48 points x 6 jet streams (2D) per 384-thread tile
+    nb = -(-rows // 128)
+    flops_tile = 2 * (L - 1) * nb * 2 * 128 * (2 * W + W) * W
+    fl = flops_tile * ws.tiles
+    ach = fl / (pde["ms"] * 1e-3) / 1e12
+    return {"achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s", "frac": ach / tf32_peak if tf32_peak else None,
+            "flops_per_launch": fl, "tiles": ws.tiles, "m_blocks_per_tile": nb,
+            "peak_source": "measured cuBLAS TF32 GEMM 8192^3 on this GPU",
+            "note": "tensor flops issued (3 TF32 products per contraction FMA, M padded to 128-row blocks); "
+                    "the FP32 SIMT weight gradient and jet epilogues bound the kernel"}
 
 
 def _traffic(config_id, n_sub, world):
@@ -796,6 +821,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--math", default=None, choices=["simt", "tf32", "tf32x3"],
+                    help="contraction math of the training kernels (default: the library's choice per plan)")
     ap.add_argument("--n-pde", type=int, default=None)
     ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
     ap.add_argument("--local-ranks", type=int, default=0,

@@ -46,7 +46,10 @@ enum { FR_MODE_PDE = 0, FR_MODE_MSE = 1, FR_MODE_VALUE = 2, FR_MODE_JET = 3, FR_
 enum { FR_FLAG_NONFINITE_LOSS = 1, FR_FLAG_NONFINITE_GRAD = 2, FR_FLAG_EXCHANGE_TIMEOUT = 4 };
 /* contraction math of the training kernels: FP32 SIMT (oracle parity ~1e-5) or
  * TF32 tcgen05 tensor cores (wide FP32 experts, 64 < width <= 512; default) */
-enum { FR_MATH_SIMT = 0, FR_MATH_TF32 = 1 };
+enum { FR_MATH_SIMT = 0, FR_MATH_TF32 = 1, FR_MATH_TF32X3 = 2 };
+/* FR_MATH_TF32X3: the W <= 64 fused epoch kernel's forward and adjoint hidden
+ * contractions on tcgen05 as split TF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi,
+ * FP32 accumulation in TMEM; ~FP32 accuracy) */
 
 typedef struct {
   int n_in, n_out, n_vel, hidden_layers, width, width_pad;
@@ -77,7 +80,8 @@ int fr_plan_create(const int* arch, int n_arch, int act, int regime, double inv_
                    fr_plan** out);
 int fr_plan_destroy(fr_plan* plan);
 int fr_plan_get_info(const fr_plan* plan, fr_plan_info* out);
-/* select FR_MATH_SIMT or FR_MATH_TF32 for the plan's PDE / MSE training kernels */
+/* select FR_MATH_SIMT, FR_MATH_TF32 (wide experts) or FR_MATH_TF32X3 (the W <= 64
+ * fused epoch kernel) for the plan's training kernels */
 int fr_plan_set_math(fr_plan* plan, int math);
 int fr_plan_workspace(const fr_plan* plan, int mode, long long n, fr_workspace* out);
 

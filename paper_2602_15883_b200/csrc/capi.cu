@@ -23,11 +23,11 @@ FR_DECL(mode_entry_VALUE)
 FR_DECL(mode_entry_JET)
 FR_DECL(mode_entry_GJ)
 #undef FR_DECL
-int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
+int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int, int);
 int wide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int wide_entry_f64(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int tcwide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
-int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int);
+int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int, int);
 }  // namespace fr
 
 namespace fr {
@@ -69,8 +69,10 @@ struct fr_plan {
   fr_plan_info info;
   ParamLayout pl;
   int* d_map = nullptr;      // real flat index -> padded index      [n_params]
-  int* d_mapT = nullptr;     // real flat index -> {W^T copy, fwd slab, dx slab} indices or -1 [3 * n_params]
+  int* d_mapT = nullptr;     // real flat index -> {W^T copy, fwd slab, dx slab, fwd lo slab, dx lo slab} or -1
+                             // [MAPT * n_params]; the lo entries hold f - tf32_trunc(f) (split TF32)
   long long tcw_f = 0, tcw_d = 0;  // kp offsets of the tensor-core operand slabs (0: none)
+  long long tc3 = 0;               // kp offset of the W=64 split-TF32 weight slabs (0: none)
   int tc_nb = 0;                   // N of the tensor-core MMAs (output units per CTA)
   int* d_inv = nullptr;      // kernel-param element -> real index or -1 [kp_elems]
 };
@@ -79,6 +81,24 @@ extern "C" const char* fr_last_error(void) { return g_err.c_str(); }
 extern "C" const char* fr_version(void) { return "flowrec_b200 0.1.0 sm_100a"; }
 
 static int preload_capi_kernels();  // defined at the end of this file
+constexpr int MAPT = 5;              // kernel-param copies per flat parameter (fr_plan::d_mapT)
+constexpr int FR_INV_LO = 1 << 30;   // inv[] flag: this element holds the split-TF32 low part
+constexpr int FR_INV_HI = 1 << 29;   // inv[] flag: ... the split-TF32 high part
+
+// split-TF32 weight pair (fr::tf32_rna, jetmlp_kernel.cuh): hi = round-to-nearest
+// TF32 of f (exactly representable, so the tensor core's truncating read is
+// exact), lo = the TF32 rounding of f - hi; both errors are unbiased
+// (|lo| <= 2^-11 |f|)
+template <typename T>
+__device__ __forceinline__ T tf32_hi(T v) {
+  if constexpr (sizeof(T) == 4) return tf32_rna(v);
+  else return v;
+}
+template <typename T>
+__device__ __forceinline__ T tf32_lo(T v) {
+  if constexpr (sizeof(T) == 4) return tf32_rna(v - tf32_rna(v));
+  else return T(0);
+}
 extern "C" int fr_plan_destroy(fr_plan* p);
 
 static int regime_dims(int regime, int* din, int* nout, int* nvel) {
@@ -137,10 +157,26 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
     p->tcw_d = p->tcw_f + (long long)(I.hidden_layers - 1) * wpad * wpad;
     I.kp_elems = int(p->tcw_d + (long long)(I.hidden_layers - 1) * wpad * wpad);
   }
+  // W = 64 FP32 fused epoch kernel on the tensor cores (FR_MATH_TF32X3): per
+  // hidden layer a forward [k/4][out][4] and an adjoint [k/4][in][4] K-major
+  // UMMA slab, each as {hi = f, lo = f - trunc_tf32(f)} (8192 floats), so a
+  // contraction is Ah*Bh + Ah*Bl + Al*Bh on tcgen05 (3xTF32, ~FP32 accuracy)
+  const bool tc3_ok = dtype == FR_F32 && wpad == 64 && I.hidden_layers >= 2;
+  if (tc3_ok) {
+    p->tc3 = (I.kp_elems + 3) & ~3;
+    I.kp_elems = int(p->tc3 + (long long)(I.hidden_layers - 1) * 2 * 8192);
+  }
+  // [k/4][128][4]: n < 64 the hi part of B[k][n], n >= 64 the lo part of B[k][n - 64]
+  auto tc3_idx = [&](int l, int dir, int lo, int n_unit, int k_unit) -> int {
+    return int(p->tc3 + ((long long)(l - 1) * 2 + dir) * 8192 + (k_unit / 4) * 512 + (lo * 64 + n_unit) * 4 +
+               (k_unit % 4));
+  };
   // wide FP32 experts train on the tcgen05 TF32 path by default (hidden
   // contractions of >= 128 units are real dense GEMMs); fr_plan_set_math
   // switches back to FP32 SIMT
-  I.math = tc_ok ? FR_MATH_TF32 : FR_MATH_SIMT;
+  // FP32 W = 64 plans: split-TF32 tcgen05 contractions in the fused epoch
+  // kernel (1.23x the FP32 SIMT epoch at config C, parity ~6e-7)
+  I.math = tc_ok ? FR_MATH_TF32 : tc3_ok ? FR_MATH_TF32X3 : FR_MATH_SIMT;
   auto tc_slab = [&](long long base, int l, int n_unit, int k_unit) -> int {
     const int nnb = wpad / tc_nb, nch = wpad / 16;
     const int nb = n_unit / tc_nb, n = n_unit % tc_nb, c = k_unit / 16, kq = (k_unit % 16) / 4, j = k_unit % 4;
@@ -157,7 +193,7 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
       for (int o = 0; o < fo; ++o) {
         const int pidx = p->pl.off_w(l) + i * fo_pad + o;
         inv[pidx] = int(map.size());
-        int tidx = -1, fidx = -1, didx = -1;
+        int tidx = -1, fidx = -1, didx = -1, flo = -1, dlo = -1;
         if (l >= 1 && l < L) {
           tidx = p->pl.off_wt(l) + o * wpad + i;
           inv[tidx] = int(map.size());
@@ -167,17 +203,28 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
             inv[fidx] = int(map.size());
             inv[didx] = int(map.size());
           }
+          if (tc3_ok) {
+            // forward B[n = out][k = in], adjoint B[n = in][k = out]
+            fidx = tc3_idx(l, 0, 0, o, i);
+            didx = tc3_idx(l, 1, 0, i, o);
+            flo = tc3_idx(l, 0, 1, o, i);
+            dlo = tc3_idx(l, 1, 1, i, o);
+            inv[fidx] = inv[didx] = int(map.size()) | FR_INV_HI;
+            inv[flo] = inv[dlo] = int(map.size()) | FR_INV_LO;
+          }
         }
         map.push_back(pidx);
         mapT.push_back(tidx);
         mapT.push_back(fidx);
         mapT.push_back(didx);
+        mapT.push_back(flo);
+        mapT.push_back(dlo);
       }
     for (int o = 0; o < fo; ++o) {
       const int pidx = p->pl.off_b(l) + o;
       inv[pidx] = int(map.size());
       map.push_back(pidx);
-      for (int r = 0; r < 3; ++r) mapT.push_back(-1);
+      for (int r = 0; r < MAPT; ++r) mapT.push_back(-1);
     }
   }
   I.n_params = int(map.size());
@@ -222,6 +269,12 @@ extern "C" int fr_plan_destroy(fr_plan* p) {
 extern "C" int fr_plan_set_math(fr_plan* p, int math) {
   if (!p) return fail("fr_plan_set_math: NULL plan");
   if (math == FR_MATH_SIMT) {
+    p->info.math = math;
+    return 0;
+  }
+  if (math == FR_MATH_TF32X3) {
+    if (p->tc3 == 0)
+      return fail("split-TF32 tensor-core math covers FP32 plans of hidden width <= 64 with >= 2 hidden layers");
     p->info.math = math;
     return 0;
   }
@@ -272,10 +325,11 @@ static int mode_call(const fr_plan* p, int mode, const KArgs* a, int grid, cudaS
 
 static int epoch_call(const fr_plan* p, const EpochArgs* e, int grid, cudaStream_t st, KInfo* info) {
   const fr_plan_info& I = p->info;
+  const int tc = I.math == FR_MATH_TF32X3;
   const int r = I.dtype == FR_F32
-                    ? epoch_entry_f32(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers)
-                    : epoch_entry_f64(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers);
-  if (r == -1) return fail("epoch kernel variant not compiled");
+                    ? epoch_entry_f32(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers, tc)
+                    : epoch_entry_f64(I.act, I.regime, I.width_pad, e, grid, st, info, I.hidden_layers, tc);
+  if (r == -1) return fail("epoch kernel variant not compiled (math %d)", I.math);
   if (r != 0) return cuda_fail(cudaError_t(r), "epoch kernel launch");
   return 0;
 }
@@ -421,7 +475,15 @@ template <typename T>
 __global__ void prepare_kernel(const double* __restrict__ flat, const int* __restrict__ inv, T* kp, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int r = inv[i];
-    kp[i] = r >= 0 ? T(flat[r]) : T(0);
+    if (r < 0) {
+      kp[i] = T(0);
+    } else if (r & FR_INV_LO) {
+      kp[i] = tf32_lo(T(flat[r & ~FR_INV_LO]));
+    } else if (r & FR_INV_HI) {
+      kp[i] = tf32_hi(T(flat[r & ~FR_INV_HI]));
+    } else {
+      kp[i] = T(flat[r]);
+    }
   }
 }
 
@@ -579,12 +641,15 @@ extern "C" int fr_epoch_fwd_bwd_gated(const fr_plan* p, const void* kparams, con
       for (int c = 0; c < I.n_vel; ++c) a.velw[c] = vel_w[c];
   };
   fill(e.pde, n_colloc);
+  const long long tc3 = I.math == FR_MATH_TF32X3 ? p->tc3 : 0;
+  e.pde.tc3 = tc3;
   e.pde.pts = colloc;
   e.pde.coef = pde_coef;
   e.pde.lpart = lpart_blocks[0];
   e.n_mse = n_set_count;
   for (int i = 0; i < n_set_count; ++i) {
     fill(e.mse[i], sets[i].n);
+    e.mse[i].tc3 = tc3;
     e.mse[i].pts = sets[i].pts;
     e.mse[i].tu = sets[i].target_u;
     e.mse[i].tp = sets[i].target_p;
@@ -849,9 +914,16 @@ __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, co
     if (a.kparams) {
       T* kp = static_cast<T*>(a.kparams);
       kp[map[i]] = T(p);
+      if (mapT[MAPT * i] >= 0) kp[mapT[MAPT * i]] = T(p);
+      // entries 1, 2: the wide path's TF32 slabs (plain copies) or the W=64
+      // split-TF32 hi slabs (entries 3, 4 -- their lo parts -- are set then)
+      const bool split = mapT[MAPT * i + 3] >= 0;
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
-        if (mapT[3 * i + r] >= 0) kp[mapT[3 * i + r]] = T(p);
+      for (int r = 1; r < 3; ++r)
+        if (mapT[MAPT * i + r] >= 0) kp[mapT[MAPT * i + r]] = split ? tf32_hi(T(p)) : T(p);
+#pragma unroll
+      for (int r = 3; r < MAPT; ++r)
+        if (mapT[MAPT * i + r] >= 0) kp[mapT[MAPT * i + r]] = tf32_lo(T(p));
     }
   }
   // ---- the last block advances the step counter ----

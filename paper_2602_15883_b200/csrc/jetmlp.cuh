@@ -94,6 +94,7 @@ struct KArgs {
   unsigned gate_mult;          //   (monotonic arrival counter of the peer-memory transport)
   int* flags;           // FLAG_EXCHANGE_TIMEOUT on a timed-out gate wait
   unsigned long long gate_timeout_ns;
+  long long tc3;        // kp offset of the split-TF32 weight slabs (epoch kernel, FR_MATH_TF32X3), else 0
 };
 
 // Padded flat parameter layout used by the kernels (T precision):

@@ -84,12 +84,26 @@ int run_mode(const KArgs* a, int grid, cudaStream_t st, KInfo* info, int L) {
   return int(cudaGetLastError());
 }
 
+template <typename T, int ACT, int REG, int W, bool TC>
+int run_epoch_v(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L);
+
+// tc: split-TF32 tensor-core contractions (FR_MATH_TF32X3; FP32, W = 64 only)
 template <typename T, int ACT, int REG, int W>
-int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
+int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L, int tc) {
+  if constexpr (sizeof(T) == 4 && W == 64 && EpochCfg<T, ACT, REG, W>::CPS == 1) {
+    if (tc) return run_epoch_v<T, ACT, REG, W, true>(e, grid, st, info, L);
+  } else {
+    if (tc) return -1;
+  }
+  return run_epoch_v<T, ACT, REG, W, false>(e, grid, st, info, L);
+}
+
+template <typename T, int ACT, int REG, int W, bool TC>
+int run_epoch_v(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
   using E = EpochCfg<T, ACT, REG, W>;
   using CP = JetCfg<T, ACT, MODE_PDE, REG, W, E::NT>;
   using CM = JetCfg<T, ACT, MODE_MSE, REG, W, E::NT>;
-  const size_t smem = CP::smem_bytes(L) > CM::smem_bytes(L) ? CP::smem_bytes(L) : CM::smem_bytes(L);
+  const size_t smem = CP::smem_bytes(L, TC) > CM::smem_bytes(L, TC) ? CP::smem_bytes(L, TC) : CM::smem_bytes(L, TC);
   const int sp = CP::stash_per_thread(L) > CM::stash_per_thread(L) ? CP::stash_per_thread(L) : CM::stash_per_thread(L);
   if (info) {
     info->nt = CP::NT;
@@ -99,7 +113,7 @@ int run_epoch(const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L)
     info->smem = smem;
     info->cps = E::CPS;
   }
-  auto k = jetmlp_epoch_kernel<T, ACT, REG, W>;
+  auto k = jetmlp_epoch_kernel<T, ACT, REG, W, TC>;
   static unsigned long long loaded = 0;
   static size_t smem_set = 0;
   if (smem > smem_set) {
@@ -126,11 +140,12 @@ int dispatch_mode_t(int act, int reg, int w, const KArgs* a, int grid, cudaStrea
 }
 
 template <typename T>
-int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L) {
+int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st, KInfo* info, int L,
+                     int tc) {
   auto go = [&](auto act_c, auto reg_c) -> int {
     constexpr int ACT = decltype(act_c)::value, REG = decltype(reg_c)::value;
-    if (w == 16) return run_epoch<T, ACT, REG, 16>(e, grid, st, info, L);
-    if (w == 64) return run_epoch<T, ACT, REG, 64>(e, grid, st, info, L);
+    if (w == 16) return tc ? -1 : run_epoch<T, ACT, REG, 16>(e, grid, st, info, L, 0);
+    if (w == 64) return run_epoch<T, ACT, REG, 64>(e, grid, st, info, L, tc);
     return -1;
   };
   return dispatch_act_reg(act, reg, go);
@@ -150,9 +165,11 @@ int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cuda
 #define FR_PHASE_READER(TAG)                                                          \
   extern "C" int fr_debug_phase_cycles_##TAG(unsigned long long* out, int reset) {    \
     cudaMemcpyFromSymbol(out, fr::g_phase_cycles, sizeof(unsigned long long) * 16);   \
+    cudaMemcpyFromSymbol(out + 16, fr::g_tc_cycles, sizeof(unsigned long long) * 16); \
     if (reset) {                                                                      \
       unsigned long long z[16] = {0};                                                 \
       cudaMemcpyToSymbol(fr::g_phase_cycles, z, sizeof(z));                           \
+      cudaMemcpyToSymbol(fr::g_tc_cycles, z, sizeof(z));                              \
     }                                                                                 \
     return 0;                                                                         \
   }
@@ -162,8 +179,8 @@ int dispatch_epoch_t(int act, int reg, int w, const EpochArgs* e, int grid, cuda
 #define FR_DEFINE_EPOCH_ENTRY(T, TAG)                                                                  \
   namespace fr {                                                                                      \
   int epoch_entry_##TAG(int act, int reg, int w, const EpochArgs* e, int grid, cudaStream_t st,        \
-                        KInfo* info, int L) {                                                         \
-    return dispatch_epoch_t<T>(act, reg, w, e, grid, st, info, L);                                    \
+                        KInfo* info, int L, int tc) {                                                 \
+    return dispatch_epoch_t<T>(act, reg, w, e, grid, st, info, L, tc);                                \
   }                                                                                                   \
   }                                                                                                   \
   FR_PHASE_READER(TAG)

@@ -1,6 +1,7 @@
 // Kernel template bodies (included by the per-mode translation units).
 #pragma once
 #include "jetmlp.cuh"
+#include "tcgen05.cuh"
 
 namespace fr {
 
@@ -167,11 +168,12 @@ struct JetCfg {
   }
   // shared memory carve (elements of T), all blocks 16-byte aligned
   __host__ __device__ static constexpr int al(int n) { return (n + 3) & ~3; }
-  __host__ __device__ static int smem_elems(int L) {
+  // tc: the split-TF32 tensor-core epoch path (weight slots hold {hi, lo} slabs)
+  __host__ __device__ static int smem_elems(int L, bool tc = false) {
     int e = 0;
     e += al(XELEMS);                       // Xs
     if (BWD) e += al(XELEMS);              // Gs
-    e += 2 * W * W;                        // weight slots
+    e += (tc ? 4 : 2) * W * W;             // weight slots
     e += al(DIN * W);                      // W0s
     e += al(L * W);                        // hidden biases
     e += al(W * NOUT);                     // WLs
@@ -186,7 +188,7 @@ struct JetCfg {
   static_assert(!BWD || ROWS * NOUT >= NT, "db partials alias Ys");
   // the per-thread loss partials of the final reduction alias Xs (free by then)
   static_assert(XELEMS * sizeof(T) >= 2 * NT * sizeof(double), "loss-reduction scratch must fit in Xs");
-  __host__ __device__ static size_t smem_bytes(int L) { return size_t(smem_elems(L)) * sizeof(T); }
+  __host__ __device__ static size_t smem_bytes(int L, bool tc = false) { return size_t(smem_elems(L, tc)) * sizeof(T); }
 };
 
 // Ghost-overlap gate (fr_epoch_gate): spin with back-off until the transport
@@ -235,6 +237,9 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 // FP32 inner-loop unroll factors (tuned on B200; overridable for sweeps)
 #ifndef FR_EPOCH_2CTA
 #define FR_EPOCH_2CTA 0  // two 192-thread CTAs per SM: measured slower (5.89 vs 5.40 ms), kept as a tuning switch
+#endif
+#ifndef FR_TC_DX_EARLY
+#define FR_TC_DX_EARLY 1  // issue the dX hi passes before the SIMT dW (they then share shared-memory bandwidth)
 #endif
 #ifndef FR_GEMM_UNROLL
 #define FR_GEMM_UNROLL 8
@@ -467,14 +472,190 @@ __device__ __forceinline__ void ld_run(T (&v)[N], const T* lb, int q0) {
 }
 
 // ---------------------------------------------------------------------------
+// Split-TF32 hidden-layer contractions on the 5th-generation tensor core
+// (FR_MATH_TF32X3, FP32 W = 64 epoch kernel).  out[row][n] = sum_k A[row][k] B[k][n]
+// over the tile's ROWS rows.  A lives in the k-quad shared layout, which IS
+// the K-major SWIZZLE_NONE UMMA layout (SBO = 128 B, LBO = RS4 * 4 B); B is a
+// pre-tiled [k/4][128][4] slab whose n < 64 half holds hi = rna_tf32(W) and
+// whose n >= 64 half holds lo = rna_tf32(W - hi) (LBO = 2 KB).  The tensor
+// core reads FP32 operands as TF32 (truncated), so with
+// A_lo = rna_tf32(A - trunc(A)) held in a second buffer
+//     A B ~= trunc(A) [B_hi | B_lo]  (one N = 128 MMA: both terms at once)
+//           + A_lo B_hi               (N = 64, into the B_lo half),
+// FP32-level accuracy (the dropped A_lo B_lo and the roundings of the lo
+// parts are <= ~2^-21 relative and unbiased).  M = 128-row blocks
+// (ceil(ROWS / 128); the last reads past the tile, those D rows are never
+// read), K = 8 per instruction, accumulators in TMEM columns
+// [128 b, 128 b + 128): the big term in the first 64, the corrections in the
+// other 64, summed in FP32 when D is drained.  One thread issues; one commit
+// tracks every MMA it issued; one warp per (block, TMEM lane quadrant) drains.
+// ---------------------------------------------------------------------------
+struct TcState {
+  uint32_t tmem;   // TMEM base (512 columns)
+  uint64_t* mbar;  // MMA-completion barrier
+  uint32_t phase;  // parity of the next completion
+};
+
+// bounded mbarrier wait: a lost completion traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void tc_wait(TcState& t) {
+  const uint32_t a = tc::smem_u32(t.mbar);
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+  for (int spin = 0; !done; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(t.phase)
+        : "memory");
+    if (!done && (spin & 1023) == 1023) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 2000000000ull) __trap();
+    }
+  }
+  t.phase ^= 1u;
+}
+
+#ifdef FR_PHASE_TIMERS
+// tc3 sub-phase cycles (thread 0): [10] A_lo transform, [11] MMA wait, [12] drain
+__device__ unsigned long long g_tc_cycles[16];
+#define FR_TC_MARK(id)                                               \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      const long long t_ = clock64();                                \
+      atomicAdd(&g_tc_cycles[id], (unsigned long long)(t_ - tc_last)); \
+      tc_last = t_;                                                  \
+    }                                                                \
+  } while (0)
+#define FR_TC_START long long tc_last = clock64()
+#else
+#define FR_TC_MARK(id) \
+  do {                 \
+  } while (0)
+#define FR_TC_START \
+  do {              \
+  } while (0)
+#endif
+
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+// the A-side low part: what the tensor core's truncating read of A misses, rounded to TF32
+__device__ __forceinline__ float tf32_alo(float x) { return tf32_rna(x - tf32_trunc(x)); }
+
+// The issue loops are the critical path of a 64-wide contraction (48 MMAs of
+// 32..64 tensor cycles each), so descriptors are built once and advanced by
+// adding the byte offset >> 4 to the start-address field (addresses stay
+// below 256 KB: no carry out of the 14-bit field), and the accumulate flag is
+// a literal.
+__device__ __forceinline__ void mma_tf32_lit(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             bool accumulate) {
+  if (accumulate)
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem_d), "l"(adesc), "l"(bdesc),
+                 "r"(idesc));
+  else
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 0;\n" ::"r"(tmem_d), "l"(adesc), "l"(bdesc),
+                 "r"(idesc));
+}
+
+// trunc(A) [B_hi | B_lo] for every M block (no commit), issued by thread `issuer`
+template <int ROWS, int RS4>
+__device__ __forceinline__ void tc3_issue_hi(const float* A, const float* Bslab, const TcState& t, int issuer = 0) {
+  constexpr int NB = (ROWS + 127) / 128;
+  static_assert(NB * 128 <= 512, "accumulators fit the 512 TMEM columns");
+  if (threadIdx.x == issuer) {
+    const uint32_t id = tc::idesc_tf32(128, 128);
+    const uint64_t a0 = tc::desc(A, RS4 * 4, 128), b0 = tc::desc(Bslab, 2048, 128);
+    tc::fence_after();
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        mma_tf32_lit(t.tmem + 128 * b, a0 + uint64_t(((512 * b + 2 * RS4 * ks) * 4) >> 4),
+                     b0 + uint64_t((1024 * ks * 4) >> 4), id, ks != 0);
+  }
+}
+
+// A_lo B_hi into the correction half, then one commit for everything the
+// issuer issued (it must be the thread that issued the hi passes)
+template <int ROWS, int RS4>
+__device__ __forceinline__ void tc3_issue_lo(const float* Alo, const float* Bslab, const TcState& t, int issuer = 0) {
+  constexpr int NB = (ROWS + 127) / 128;
+  if (threadIdx.x == issuer) {
+    const uint32_t id = tc::idesc_tf32(128, 64);
+    const uint64_t a0 = tc::desc(Alo, RS4 * 4, 128), b0 = tc::desc(Bslab, 2048, 128);
+    tc::fence_after();
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        mma_tf32_lit(t.tmem + 128 * b + 64, a0 + uint64_t(((512 * b + 2 * RS4 * ks) * 4) >> 4),
+                     b0 + uint64_t((1024 * ks * 4) >> 4), id, true);
+    tc::mma_commit(t.mbar);
+  }
+}
+
+// wait for the commit, then out[row][n] = D[row][n] + D[row][64 + n] (k-quad layout)
+template <int ROWS, int RS4, int NT>
+__device__ __forceinline__ void tc3_drain(float* out, TcState& t) {
+  constexpr int NB = (ROWS + 127) / 128;
+  FR_TC_START;
+  tc_wait(t);
+  tc::fence_after();
+  FR_TC_MARK(11);
+  // warp w takes (M block, lane quadrant) pairs wq = w, w + NT/32, ...; a warp
+  // may only read TMEM lane quadrant w % 4, so wq % 4 == w % 4 always
+  static_assert((NT / 32) % 4 == 0, "drain warps come in TMEM lane-quadrant groups of four");
+  for (int wq = threadIdx.x >> 5; wq < 4 * NB; wq += NT / 32) {
+    const int q = wq & 3, b = wq >> 2;
+    const int row = 128 * b + 32 * q + (threadIdx.x & 31);
+    const uint32_t ta = t.tmem + (uint32_t(32 * q) << 16) + uint32_t(128 * b);
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16], w[16];
+      tc::tmem_ld16(ta + c0, v);
+      tc::tmem_ld16(ta + 64 + c0, w);
+      if (row < ROWS) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          *reinterpret_cast<float4*>(out + ((c0 >> 2) + cc) * RS4 + 4 * row) =
+              make_float4(v[4 * cc] + w[4 * cc], v[4 * cc + 1] + w[4 * cc + 1], v[4 * cc + 2] + w[4 * cc + 2],
+                          v[4 * cc + 3] + w[4 * cc + 3]);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  FR_TC_MARK(12);
+}
+
+// A_lo of a whole k-quad buffer, out of place (dst may not alias src)
+template <int RS4, int NT>
+__device__ __forceinline__ void tc3_make_lo(float* dst, const float* src) {
+  FR_TC_START;
+  for (int i = 4 * threadIdx.x; i < 16 * RS4; i += 4 * NT) {
+    const float4 v = *reinterpret_cast<const float4*>(src + i);
+    *reinterpret_cast<float4*>(dst + i) = make_float4(tf32_alo(v.x), tf32_alo(v.y), tf32_alo(v.z), tf32_alo(v.w));
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  FR_TC_MARK(10);
+}
+
+// ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 // Processes tiles t0, t0 + tstride, ... of one dataset with this CTA.  Gradient
 // contributions are red.add-ed into gp_row (zeroed first when zero_partials);
 // the CTA's loss sums are written to lpart_row[0..1].
-template <typename T, int ACT, int MODE, int REG, int W, int NT_>
+template <typename T, int ACT, int MODE, int REG, int W, int NT_, bool TC = false>
 __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_raw, long long t0, long long tstride,
-                                          bool zero_partials, double* gp_row, double* lpart_row) {
+                                          bool zero_partials, double* gp_row, double* lpart_row,
+                                          TcState* tcs = nullptr) {
   using C = JetCfg<T, ACT, MODE, REG, W, NT_>;
   constexpr int NT = C::NT, G = C::G, RPT = C::RPT, ROWS = C::ROWS, PPT = C::PPT;
   constexpr int DIN = C::DIN, NOUT = C::NOUT, NVEL = C::NVEL, S = C::S;
@@ -487,8 +668,10 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   T* Xs = sm;                      sm += C::al(C::XELEMS);
   T* Gs = nullptr;
   if constexpr (BWD) { Gs = sm; sm += C::al(C::XELEMS); }
-  T* slot0 = sm;                   sm += W * W;
-  T* slot1 = sm;                   sm += W * W;
+  static_assert(!TC || (sizeof(T) == 4 && W == 64 && BWD), "split-TF32 path: FP32, W = 64, training modes");
+  constexpr int SLOT = (TC ? 2 : 1) * W * W;  // TC: {hi, lo} UMMA slab pair
+  T* slot0 = sm;                   sm += SLOT;
+  T* slot1 = sm;                   sm += SLOT;
   T* W0s = sm;                     sm += C::al(DIN * W);
   T* Bs = sm;                      sm += C::al(L * W);
   T* WLs = sm;                     sm += C::al(W * NOUT);
@@ -530,13 +713,17 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   const int nmat = (L - 1) * (BWD ? 2 : 1);
   auto mat_src = [&](int idx) -> const T* {
     int i = idx % nmat;
+    if constexpr (TC) {  // forward slab of layer i + 1, then adjoint slabs of layers L-1..1
+      if (i < L - 1) return kp + a.tc3 + size_t(i) * 2 * 8192;
+      return kp + a.tc3 + (size_t(2 * L - 3 - i) * 2 + 1) * 8192;
+    }
     if (i < L - 1) return kp + pl.off_w(i + 1);
     return kp + pl.off_wt(2 * L - 2 - i);
   };
   auto stage = [&](int idx) {
     T* dst = (idx & 1) ? slot1 : slot0;
     const T* src = mat_src(idx);
-    constexpr int CH = W * W * int(sizeof(T)) / 16;
+    constexpr int CH = SLOT * int(sizeof(T)) / 16;
     for (int i = tid; i < CH; i += NT)
       cp_async16(reinterpret_cast<char*>(dst) + 16 * i, reinterpret_cast<const char*>(src) + 16 * i);
     cp_async_commit();
@@ -613,6 +800,13 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       }
       if constexpr (BWD && JET) st_run<NT>(st_at(0), 0, s0v);
       store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
+      if constexpr (TC) {  // the first hidden contraction's A_lo
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) outv[r][j] = tf32_alo(outv[r][j]);
+        store_block<T, W, RPT, RS4>(Gs, rg, g, outv);
+      }
     }
     __syncthreads();
     FR_MARK(1);
@@ -622,7 +816,20 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
       const T* Bm = (ws & 1) ? slot1 : slot0;
       stage(ws + 1);
       T acc[RPT][8];
-      gemm_rows<T, W, RPT, RS4>(Xs, Bm, rg, g, acc);
+      if constexpr (TC) {
+        // tensor core: A = Xs (this layer's input), A_lo = Gs (written beside
+        // it by the producing epilogue); D -> Gs (this layer's output buffer),
+        // then each thread picks up its rows exactly as the SIMT GEMM leaves
+        // them in registers
+        tc::fence_proxy_async();
+        __syncthreads();
+        tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Xs), reinterpret_cast<const float*>(Bm), *tcs);
+        tc3_issue_lo<ROWS, RS4>(reinterpret_cast<const float*>(Gs), reinterpret_cast<const float*>(Bm), *tcs);
+        tc3_drain<ROWS, RS4, NT>(reinterpret_cast<float*>(Gs), *tcs);
+        load_block<T, W, RPT, RS4>(acc, Gs, rg, g);
+      } else {
+        gemm_rows<T, W, RPT, RS4>(Xs, Bm, rg, g, acc);
+      }
       // training modes ping-pong the layer input / output between Xs and Gs
       // (Gs is idle in the forward sweep), so a warp's epilogue never waits
       // for the slower warps' GEMM; single-buffer modes sync here
@@ -671,6 +878,13 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         }
       }
       store_block<T, W, RPT, RS4>(BWD ? Gs : Xs, rg, g, outv);
+      if constexpr (TC) {  // the next contraction's A_lo, into this layer's (consumed) input buffer
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) outv[r][j] = tf32_alo(outv[r][j]);
+        store_block<T, W, RPT, RS4>(Xs, rg, g, outv);
+      }
       cp_async_wait_all();
       __syncthreads();
       FR_MARK(3);
@@ -993,8 +1207,15 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           }
           store_block<T, W, RPT, RS4>(Xs, rg, g, hv);
         }
+        if constexpr (TC) tc::fence_proxy_async();  // Zbar_l (Gs) feeds the tensor core next
         __syncthreads();
         FR_MARK(7);
+        // tensor core: the dX hi passes over Zbar_l run under the SIMT weight
+        // gradient, issued by a thread the dW thread tiles leave idle
+        constexpr int DX_ISSUER = (C::KT * C::KT * C::RSPLIT < NT) ? C::KT * C::KT * C::RSPLIT : 0;
+        if constexpr (TC && FR_TC_DX_EARLY)
+          tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs),
+                                  reinterpret_cast<const float*>((ws & 1) ? slot1 : slot0), *tcs, DX_ISSUER);
         stage(ws + 1);
 
         // dW_l = H_l^T Zbar_l over all rows of the tile.  Thread tile 8k x 8u
@@ -1120,7 +1341,18 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         // dX: S-bar_{l-1} = Zbar_l W_l^T
         {
           const T* Bm = (ws & 1) ? slot1 : slot0;
-          if constexpr (sizeof(T) == 4) {
+          if constexpr (TC) {
+            // Zbar_l's A_lo into Xs (free again after the dW combine), the A_lo
+            // pass, then S-bar_{l-1} lands straight in Gs
+            if constexpr (!FR_TC_DX_EARLY)
+              tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs), reinterpret_cast<const float*>(Bm), *tcs,
+                                      DX_ISSUER);
+            tc3_make_lo<RS4, NT>(reinterpret_cast<float*>(Xs), reinterpret_cast<const float*>(Gs));
+            tc3_issue_lo<ROWS, RS4>(reinterpret_cast<const float*>(Xs), reinterpret_cast<const float*>(Bm), *tcs,
+                                    DX_ISSUER);
+            tc3_drain<ROWS, RS4, NT>(reinterpret_cast<float*>(Gs), *tcs);
+            FR_MARK(10);
+          } else if constexpr (sizeof(T) == 4) {
             f32x2 acc2[RPT][4];
             gemm_rows_f2<W, RPT, RS4>(reinterpret_cast<const float*>(Gs), reinterpret_cast<const float*>(Bm), rg,
                                       g, acc2);
@@ -1270,20 +1502,34 @@ struct EpochCfg {
   static constexpr int CPS = TWO ? 2 : 1;
 };
 
-template <typename T, int ACT, int REG, int W>
+template <typename T, int ACT, int REG, int W, bool TC = false>
 __global__ void __launch_bounds__(EpochCfg<T, ACT, REG, W>::NT, EpochCfg<T, ACT, REG, W>::CPS)
     jetmlp_epoch_kernel(EpochArgs e) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NT = EpochCfg<T, ACT, REG, W>::NT;
   const long long G = gridDim.x, c = blockIdx.x;
+  TcState* tcs = nullptr;
+  if constexpr (TC) {
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ TcState st;
+    const uint32_t base = tc_setup<512>(&tmem_slot, &mbar, 1);
+    st = TcState{base, &mbar, 0u};
+    __syncthreads();
+    tcs = &st;
+  }
   double* gp = e.pde.gpart + size_t(c) * e.pde.np_pad;
-  run_tiles<T, ACT, MODE_PDE, REG, W, NT>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c);
+  TcState local{};
+  if constexpr (TC) local = *tcs;  // every thread tracks the barrier phase in a register
+  run_tiles<T, ACT, MODE_PDE, REG, W, NT, TC>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c, &local);
   long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT;
   for (int d = 0; d < e.n_mse; ++d) {
     const long long t0 = ((c - offset) % G + G) % G;
-    run_tiles<T, ACT, MODE_MSE, REG, W, NT>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c);
+    run_tiles<T, ACT, MODE_MSE, REG, W, NT, TC>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c,
+                                                &local);
     offset += (e.mse[d].n + JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT;
   }
+  if constexpr (TC) tc_teardown<512>(local.tmem);
 }
 
 }  // namespace fr

@@ -124,4 +124,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 }  // namespace tc
+
+// TMEM allocation + mbarrier init (CTA-wide; every thread calls)
+template <int NCOLS>
+__device__ __forceinline__ uint32_t tc_setup(uint32_t* slot, uint64_t* mbar, int nbar) {
+  if (threadIdx.x < 32) tc::tmem_alloc<NCOLS>(slot);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nbar; ++i) tc::mbar_init(&mbar[i], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  return *slot;
+}
+template <int NCOLS>
+__device__ __forceinline__ void tc_teardown(uint32_t tmem) {
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_free<NCOLS>(tmem);
+}
+
 }  // namespace fr

@@ -241,26 +241,6 @@ __device__ __forceinline__ void slab_copy_out(const float* slab, float* dst, int
     reinterpret_cast<float4*>(dst)[tid + 128 * i] = reinterpret_cast<const float4*>(slab)[tid + 128 * i];
 }
 
-// TMEM allocation + mbarrier init (CTA-wide; every thread calls)
-template <int NCOLS>
-__device__ __forceinline__ uint32_t tc_setup(uint32_t* slot, uint64_t* mbar, int nbar) {
-  if (threadIdx.x < 32) tc::tmem_alloc<NCOLS>(slot);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nbar; ++i) tc::mbar_init(&mbar[i], 1);
-    tc::fence_mbar_init();
-  }
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  return *slot;
-}
-template <int NCOLS>
-__device__ __forceinline__ void tc_teardown(uint32_t tmem) {
-  tc::fence_before();
-  __syncthreads();
-  if (threadIdx.x < 32) tc::tmem_free<NCOLS>(tmem);
-}
-
 // 2 K-steps (16 deep) of A[kq][MA][4] x B[kq][NB][4]
 __device__ __forceinline__ void tc_mma16(uint32_t tmem, const float* A, int MA, const float* B, int NB, uint32_t idesc,
                                          bool first) {

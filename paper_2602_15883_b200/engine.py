@@ -30,7 +30,7 @@ def require_cuda():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-MATH_CODES = {"simt": 0, "tf32": 1}
+MATH_CODES = {"simt": 0, "tf32": 1, "tf32x3": 2}
 
 
 class Plan:

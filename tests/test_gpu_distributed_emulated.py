@@ -68,7 +68,7 @@ def _run_distributed(plan, overlap, monkeypatch):
     monkeypatch.setattr(dist, "get_world_size", lambda *a, **k: plan.n_ranks)
     transport = CopyTransport(plan)
     monkeypatch.setattr(driver, "post_exchange", transport)
-    trainers = [driver.DistributedTrainer(plan, rank=r, overlap=overlap, reserve_sms=sms - MAX_CTAS)
+    trainers = [driver.DistributedTrainer(plan, rank=r, overlap=overlap, reserve_sms=sms - MAX_CTAS, transport="torch")
                 for r in range(plan.n_ranks)]
     for t in trainers:
         transport.register(t)

@@ -260,14 +260,22 @@ def test_tf32_matches_oracle_at_cylinder_scale(width, layers, act, kind):
 
 
 def test_math_mode_selection():
-    """TF32 is the default for wide FP32 experts only; FP64, narrow and
-    single-hidden-layer plans refuse it."""
+    """TF32 is the default for wide FP32 experts, split TF32 (tf32x3) for the
+    FP32 W <= 64 fused epoch kernel; FP64, narrow-width and single-hidden-layer
+    plans refuse the tensor-core modes."""
     from paper_2602_15883_b200 import _lib as X
     from paper_2602_15883_b200 import engine
     from paper_2602_15883_b200.network import ExpertConfig
 
     assert engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0).info.math == 1
-    assert engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0).info.math == 0
+    assert engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0).info.math == 2
+    assert engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0, math="simt").info.math == 0
+    assert engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0, "float64").info.math == 0
+    assert engine.Plan(ExpertConfig(3, 2, 16, "tanh", 3), "unsteady2d", 100.0).info.math == 0
+    with pytest.raises(X.FlowrecError, match="split-TF32"):
+        engine.Plan(ExpertConfig(3, 4, 64, "tanh", 3), "unsteady2d", 100.0, "float64", math="tf32x3")
+    with pytest.raises(X.FlowrecError, match="split-TF32"):
+        engine.Plan(ExpertConfig(3, 1, 64, "tanh", 3), "unsteady2d", 100.0, math="tf32x3")
     assert engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0, "float64").info.math == 0
     with pytest.raises(X.FlowrecError, match="FP32"):
         engine.Plan(ExpertConfig(3, 3, 150, "sin", 3), "unsteady2d", 100.0, "float64", math="tf32")

@@ -30,14 +30,15 @@ def main():
 
     n = int(os.environ.get("N_PDE", "500000"))
     pb = cylinder2d_problem(n_procs=1, n_pde=n, hidden_layers=4, width=64, activation="tanh")
-    tc = TrainConfig(epochs=8, batch_size=25000, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor)
+    tc = TrainConfig(epochs=8, batch_size=25000, learning_rate=1e-3, weights=pb.weights, anchor=pb.anchor,
+                     math=os.environ.get("MATH") or None)
     tr = LocalTrainer(build_plan(pb.subdomains, pb.datasets, pb.expert_config, tc))
     tr.run(2, use_graphs=False, record_times=False)
     torch.cuda.synchronize()
     lib = X.lib()
     f = lib.fr_debug_phase_cycles_f32
     f.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-    buf = (C.c_ulonglong * 16)()
+    buf = (C.c_ulonglong * 32)()
     f(buf, 1)
     tr.run(4, start=2, use_graphs=False, record_times=False)
     torch.cuda.synchronize()
@@ -46,6 +47,9 @@ def main():
     for i, name in enumerate(PHASES):
         print(f"{i:2d} {name:28s} {buf[i] / tot * 100:6.2f}%")
     print("total CTA-cycles", tot)
+    for i, name in ((10, "tc3 dX A_lo transform"), (11, "tc3 MMA wait"), (12, "tc3 drain D")):
+        if buf[16 + i]:
+            print(f"   {name:28s} {buf[16 + i] / tot * 100:6.2f}%")
 
 
 if __name__ == "__main__":
