@@ -238,6 +238,16 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 #ifndef FR_EPOCH_2CTA
 #define FR_EPOCH_2CTA 0  // two 192-thread CTAs per SM: measured slower (5.89 vs 5.40 ms), kept as a tuning switch
 #endif
+#ifndef FR_TC_DW
+// tensor-core weight gradient (tc3_dw): correct, but with only the idle weight
+// slot (32 KB) to stage the transposed operands it runs 16-row chunks
+// double-buffered and is bound by the MMA -> commit round trip: measured 16.6k
+// vs 13.7k cycles per tile-layer for the SIMT dW, so off
+#define FR_TC_DW 0
+#endif
+#ifndef FR_DW_SPLIT6
+#define FR_DW_SPLIT6 0  // TC epoch: SIMT dW over 6 row ranges (all 12 warps): measured 1.5% slower, off
+#endif
 #ifndef FR_TC_DX_EARLY
 #define FR_TC_DX_EARLY 1  // issue the dX hi passes before the SIMT dW (they then share shared-memory bandwidth)
 #endif
@@ -491,12 +501,35 @@ __device__ __forceinline__ void ld_run(T (&v)[N], const T* lb, int q0) {
 // tracks every MMA it issued; one warp per (block, TMEM lane quadrant) drains.
 // ---------------------------------------------------------------------------
 struct TcState {
-  uint32_t tmem;   // TMEM base (512 columns)
-  uint64_t* mbar;  // MMA-completion barrier
-  uint32_t phase;  // parity of the next completion
+  uint32_t tmem;      // TMEM base (512 columns)
+  uint64_t* mbar;     // MMA-completion barrier
+  uint32_t phase;     // parity of the next completion
+  uint64_t* mbar_dw;  // weight-gradient chunk barriers [2] (one per staging buffer)
+  uint32_t dw_phase;  // their next-completion parities (bit b = buffer b)
 };
 
 // bounded mbarrier wait: a lost completion traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* mbar, uint32_t parity) {
+  const uint32_t a = tc::smem_u32(mbar);
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+  for (int spin = 0; !done; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (!done && (spin & 1023) == 1023) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 2000000000ull) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ void tc_wait(TcState& t) {
   const uint32_t a = tc::smem_u32(t.mbar);
   uint32_t done = 0;
@@ -633,10 +666,107 @@ __device__ __forceinline__ void tc3_drain(float* out, TcState& t) {
   FR_TC_MARK(12);
 }
 
+// Weight gradient of one hidden layer on the tensor core:
+//     dW[i][o] = sum_rows H[row][i] Zbar[row][o]
+// with K = rows.  TF32 operands must be K-major, i.e. rows contiguous -- the
+// transpose of the k-quad layout -- so the tile's rows are staged 16 at a time
+// into two 16 KB buffers (double-buffered against the MMAs):
+//     A = [H^T_hi ; H^T_lo]  (M = 128: in-units hi, then lo)   [4 row quads][128][4]
+//     B = [Zbar^T_hi ; Zbar^T_lo] (N = 128: out-units hi, then lo)
+// and ONE M = N = 128 MMA per 8 rows yields every split product at once:
+// D[i][o] = H_hi Z_hi, D[i][64 + o] = H_hi Z_lo, D[64 + i][o] = H_lo Z_hi (the
+// fourth quadrant, H_lo Z_lo, is dropped).  The accumulator lives in TMEM
+// columns [384, 512) for the whole tile; the three quadrants are summed in
+// FP32 and red.add-ed into the CTA's f64 gradient row once per tile.  (hi is
+// the raw FP32 value, which the tensor core reads truncated; lo =
+// rna_tf32(x - trunc(x)).)  `stg` is the idle weight slot (32 KB), `scratch`
+// 4096 floats (free once the chunks are staged).
+template <int ROWS, int RS4, int NT, int W>
+__device__ __forceinline__ void tc3_dw(const float* H, const float* Zb, float* stg, float* scratch, double* gp_w,
+                                       TcState& t, int issuer) {
+  static_assert(W == 64 && ROWS % 16 == 0, "tensor-core weight gradient: W = 64, 16-row chunks");
+  constexpr int NCH = ROWS / 16;
+  constexpr uint32_t DCOL = 384;
+  const int tid = threadIdx.x;
+  const uint32_t id = tc::idesc_tf32(128, 128);
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c) {
+    const int b = c & 1;
+    float* buf = stg + 4096 * b;
+    if (c >= 2) {  // the chunk-(c-2) MMAs must be done with this buffer
+      mbar_wait_bounded(t.mbar_dw + b, (t.dw_phase >> b) & 1u);
+      t.dw_phase ^= 1u << b;
+    }
+    const int r0 = 16 * c;
+    for (int it = tid; it < 512; it += NT) {
+      const int which = it >> 8, rq = (it >> 6) & 3, u = it & 63;
+      const float* src = which ? Zb : H;
+      const float* sp = src + (u >> 2) * RS4 + (r0 + 4 * rq) * 4 + (u & 3);
+      const float4 v = make_float4(sp[0], sp[4], sp[8], sp[12]);
+      float* dst = buf + 2048 * which + (rq * 128 + u) * 4;
+      *reinterpret_cast<float4*>(dst) = v;
+      *reinterpret_cast<float4*>(dst + 256) = make_float4(tf32_alo(v.x), tf32_alo(v.y), tf32_alo(v.z), tf32_alo(v.w));
+    }
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == issuer) {
+      tc::fence_after();
+      const uint64_t a0 = tc::desc(buf, 2048, 128), b0 = tc::desc(buf + 2048, 2048, 128);
+      mma_tf32_lit(t.tmem + DCOL, a0, b0, id, c != 0);
+      mma_tf32_lit(t.tmem + DCOL, a0 + uint64_t(4096 >> 4), b0 + uint64_t(4096 >> 4), id, true);
+      tc::mma_commit(t.mbar_dw + b);
+    }
+  }
+  // the last two chunks' completions (the last covers every MMA before it)
+#pragma unroll
+  for (int k = NCH >= 2 ? NCH - 2 : 0; k < NCH; ++k) {
+    const int b = k & 1;
+    mbar_wait_bounded(t.mbar_dw + b, (t.dw_phase >> b) & 1u);
+    t.dw_phase ^= 1u << b;
+  }
+  tc::fence_after();
+  // drain: lanes 64..127 (H_lo Z_hi) into shared memory [o][i] (stride 65:
+  // conflict-free both ways), lanes 0..63 add H_hi Z_hi + H_hi Z_lo to it, then
+  // every thread red.adds a coalesced run of the 64 x 64 block once
+  const int w = tid >> 5, q = w & 3;
+  if (w < 4 && q >= 2) {
+    const int i = 32 * (q - 2) + (tid & 31);
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(t.tmem + (uint32_t(32 * q) << 16) + DCOL + c0, v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) scratch[(c0 + k) * 65 + i] = v[k];
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (w < 4 && q < 2) {
+    const int i = 32 * q + (tid & 31);
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16], z[16];
+      tc::tmem_ld16(t.tmem + (uint32_t(32 * q) << 16) + DCOL + c0, v);
+      tc::tmem_ld16(t.tmem + (uint32_t(32 * q) << 16) + DCOL + 64 + c0, z);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) scratch[(c0 + k) * 65 + i] += v[k] + z[k];
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  for (int e = tid; e < W * W; e += NT) {
+    const int i = e / W, o = e % W;
+    red_add(gp_w + e, double(scratch[o * 65 + i]));
+  }
+  __syncthreads();
+}
+
 // A_lo of a whole k-quad buffer, out of place (dst may not alias src)
 template <int RS4, int NT>
 __device__ __forceinline__ void tc3_make_lo(float* dst, const float* src) {
   FR_TC_START;
+  __syncthreads();  // dst may still be read by the caller's previous phase (the dW combine reads Xs)
   for (int i = 4 * threadIdx.x; i < 16 * RS4; i += 4 * NT) {
     const float4 v = *reinterpret_cast<const float4*>(src + i);
     *reinterpret_cast<float4*>(dst + i) = make_float4(tf32_alo(v.x), tf32_alo(v.y), tf32_alo(v.z), tf32_alo(v.w));
@@ -1212,19 +1342,61 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         FR_MARK(7);
         // tensor core: the dX hi passes over Zbar_l run under the SIMT weight
         // gradient, issued by a thread the dW thread tiles leave idle
-        constexpr int DX_ISSUER = (C::KT * C::KT * C::RSPLIT < NT) ? C::KT * C::KT * C::RSPLIT : 0;
-        if constexpr (TC && FR_TC_DX_EARLY)
+        // tensor-core MMAs of the backward layer: issued by a thread the SIMT
+        // dW leaves idle (or, with the tensor-core dW, by the last warp, which
+        // has the least staging work)
+        // TC: the SIMT dW may spread over 6 row ranges (all 12 warps), its 5th
+        // and 6th partials parked in the idle weight slot (the next matrix is
+        // then prefetched after the combine)
+        constexpr bool TC_DW = TC && FR_TC_DW;
+        constexpr int RSPLIT_DW = (TC && !TC_DW && FR_DW_SPLIT6 && ROWS % 6 == 0 && C::KT * C::KT * 6 == NT &&
+                                   C::XELEMS / (W * W) + 2 >= 6)
+                                      ? 6 : C::RSPLIT;
+        constexpr bool SLOT_PARTIALS = RSPLIT_DW * W * W > C::XELEMS;
+        constexpr int DX_ISSUER = TC_DW ? NT - 32
+                                  : (C::KT * C::KT * RSPLIT_DW < NT) ? C::KT * C::KT * RSPLIT_DW : 0;
+        constexpr bool DX_EARLY = TC && FR_TC_DX_EARLY && C::KT * C::KT * RSPLIT_DW < NT;
+        if constexpr (DX_EARLY)
           tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs),
                                   reinterpret_cast<const float*>((ws & 1) ? slot1 : slot0), *tcs, DX_ISSUER);
-        stage(ws + 1);
+        if constexpr (TC_DW) {
+          // weight gradient on the tensor core, staged through the idle weight
+          // slot (the next matrix is prefetched after it); db_l on the SIMT side
+          tc3_dw<ROWS, RS4, NT, W>(reinterpret_cast<const float*>(Xs), reinterpret_cast<const float*>(Gs),
+                                   reinterpret_cast<float*>((ws & 1) ? slot0 : slot1), reinterpret_cast<float*>(Xs),
+                                   gp + pl.off_w(l), *tcs, DX_ISSUER);
+          FR_MARK(8);
+          {
+            constexpr int NH = NT / W;
+            const int u = tid % W, h = tid / W;
+            T sb = T(0);
+            for (int pt = h; pt < PPT; pt += NH) sb += Gs[kqi<RS4>(JET ? pt * S : pt, u)];
+            Dbs[tid] = sb;
+          }
+          __syncthreads();
+          if (tid < W) {
+            T sb = Dbs[tid];
+#pragma unroll
+            for (int h = 1; h < NT / W; ++h) sb += Dbs[h * W + tid];
+            red_add(gp + pl.off_b(l) + tid, double(sb));
+          }
+          FR_MARK(9);
+        }
+        if constexpr (!SLOT_PARTIALS) stage(ws + 1);
 
         // dW_l = H_l^T Zbar_l over all rows of the tile.  Thread tile 8k x 8u
         // (k quads {kt, kt+W/8}, u quads {ut, ut+W/8}) over one of RSPLIT row
         // ranges; a quarter-warp shares kt (broadcast H) and spans 8 ut (one
         // conflict-free 128-byte Zbar segment).  Row-range partials are combined
         // through shared memory in a fixed order, then red.add-ed once.
-        {
-          constexpr int KT = C::KT, RSPLIT = C::RSPLIT, RROWS = ROWS / RSPLIT;
+        if constexpr (!TC_DW) {
+          constexpr int KT = C::KT, RSPLIT = RSPLIT_DW, RROWS = ROWS / RSPLIT;
+          // row-range partial rs: Xs, or (SLOT_PARTIALS) the idle weight slot past Xs' capacity
+          T* const pslot = (ws & 1) ? slot0 : slot1;
+          auto part = [&](int q) -> T* {
+            constexpr int INXS = C::XELEMS / (W * W);
+            return (!SLOT_PARTIALS || q < INXS) ? Xs + q * W * W : pslot + (q - INXS) * W * W;
+          };
           const bool active = tid < KT * KT * RSPLIT;
           const int ut = tid % KT, kt = (tid / KT) % KT, rs = tid / (KT * KT);
           T acc[8][8];
@@ -1300,7 +1472,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           // slice of the 64x64 block over rs = 0, 1, ... (fixed order) and
           // red.adds it once
           auto kidx = [&](int x) { return x < 4 ? 4 * kt + x : 4 * (kt + KT) + (x - 4); };
-          static_assert(RSPLIT == 1 || RSPLIT * W * W <= C::XELEMS, "dW row-range partials must fit in Xs");
+          static_assert(RSPLIT == 1 || RSPLIT <= C::XELEMS / (W * W) + (SLOT_PARTIALS ? 2 : 0),
+                        "dW row-range partials must fit in Xs (+ the idle weight slot)");
           if constexpr (RSPLIT == 1) {
             // one row range: every dW element has exactly one owner thread,
             // which red.adds its 8x8 block straight from registers
@@ -1313,7 +1486,7 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
                   red_add(dst + kidx(x) * W + (y < 4 ? 4 * ut + y : 4 * (ut + KT) + (y - 4)), double(acc[x][y]));
             }
           } else if (active) {
-            T* dst = Xs + rs * W * W;
+            T* dst = part(rs);
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
               vstore(dst + kidx(x) * W + 4 * ut, *reinterpret_cast<const T(*)[4]>(&acc[x][0]));
@@ -1322,6 +1495,9 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           }
           FR_MARK(9);
           __syncthreads();
+          if constexpr (TC && !DX_EARLY)  // no idle thread during dW: the dX hi passes start now
+            tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs),
+                                    reinterpret_cast<const float*>((ws & 1) ? slot1 : slot0), *tcs, DX_ISSUER);
           if (tid < W) {
             T sb = Dbs[tid];
 #pragma unroll
@@ -1331,11 +1507,15 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           if constexpr (RSPLIT > 1) {
             double* dst = gp + pl.off_w(l);
             for (int e = tid; e < W * W; e += NT) {
-              T sum = Xs[e];
+              T sum = part(0)[e];
 #pragma unroll
-              for (int q = 1; q < RSPLIT; ++q) sum += Xs[q * W * W + e];
+              for (int q = 1; q < RSPLIT; ++q) sum += part(q)[e];
               red_add(dst + e, double(sum));
             }
+          }
+          if constexpr (SLOT_PARTIALS) {
+            __syncthreads();  // the partials in the idle slot are consumed
+            stage(ws + 1);
           }
         }
         // dX: S-bar_{l-1} = Zbar_l W_l^T
@@ -1344,9 +1524,6 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           if constexpr (TC) {
             // Zbar_l's A_lo into Xs (free again after the dW combine), the A_lo
             // pass, then S-bar_{l-1} lands straight in Gs
-            if constexpr (!FR_TC_DX_EARLY)
-              tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs), reinterpret_cast<const float*>(Bm), *tcs,
-                                      DX_ISSUER);
             tc3_make_lo<RS4, NT>(reinterpret_cast<float*>(Xs), reinterpret_cast<const float*>(Gs));
             tc3_issue_lo<ROWS, RS4>(reinterpret_cast<const float*>(Xs), reinterpret_cast<const float*>(Bm), *tcs,
                                     DX_ISSUER);
@@ -1511,10 +1688,10 @@ __global__ void __launch_bounds__(EpochCfg<T, ACT, REG, W>::NT, EpochCfg<T, ACT,
   TcState* tcs = nullptr;
   if constexpr (TC) {
     __shared__ uint32_t tmem_slot;
-    __shared__ __align__(8) uint64_t mbar;
+    __shared__ __align__(8) uint64_t mbar[3];
     __shared__ TcState st;
-    const uint32_t base = tc_setup<512>(&tmem_slot, &mbar, 1);
-    st = TcState{base, &mbar, 0u};
+    const uint32_t base = tc_setup<512>(&tmem_slot, mbar, 3);
+    st = TcState{base, &mbar[0], 0u, &mbar[1], 0u};
     __syncthreads();
     tcs = &st;
   }
