@@ -648,16 +648,20 @@ __device__ __forceinline__ void tc3_drain(float* out, TcState& t) {
     const int row = 128 * b + 32 * q + (threadIdx.x & 31);
     const uint32_t ta = t.tmem + (uint32_t(32 * q) << 16) + uint32_t(128 * b);
 #pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      float v[16], w[16];
-      tc::tmem_ld16(ta + c0, v);
-      tc::tmem_ld16(ta + 64 + c0, w);
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      // both halves' loads in flight before one wait
+      uint32_t v[32], w[32];
+      tc::tmem_ld32_nowait(ta + c0, v);
+      tc::tmem_ld32_nowait(ta + 64 + c0, w);
+      tc::tmem_wait();
       if (row < ROWS) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
+        for (int cc = 0; cc < 8; ++cc)
           *reinterpret_cast<float4*>(out + ((c0 >> 2) + cc) * RS4 + 4 * row) =
-              make_float4(v[4 * cc] + w[4 * cc], v[4 * cc + 1] + w[4 * cc + 1], v[4 * cc + 2] + w[4 * cc + 2],
-                          v[4 * cc + 3] + w[4 * cc + 3]);
+              make_float4(__uint_as_float(v[4 * cc]) + __uint_as_float(w[4 * cc]),
+                          __uint_as_float(v[4 * cc + 1]) + __uint_as_float(w[4 * cc + 1]),
+                          __uint_as_float(v[4 * cc + 2]) + __uint_as_float(w[4 * cc + 2]),
+                          __uint_as_float(v[4 * cc + 3]) + __uint_as_float(w[4 * cc + 3]));
       }
     }
   }
