@@ -15,9 +15,6 @@ round-to-nearest errors cancel.  Measured (profiles/r2_parity_errors.jsonl):
 SIMT  history 2.0e-3 per term (max over epochs), params 1.5e-5, jumps 1.8e-3, fields 1.8e-6;
 TF32x3 history 5.2e-2, params 3.9e-4, jumps 5.4e-2, fields 2.0e-4."""
 
-# (history per term, params, interface jumps, field errors)
-TOL = {"simt": (1e-2, 1e-4, 1e-2, 1e-4), None: (1e-1, 1e-3, 1e-1, 1e-3)}
-
 import os
 
 import numpy as np
@@ -27,6 +24,8 @@ from conftest import ROOT, per_term_rel, rel_l2, report
 
 pytestmark = pytest.mark.gpu
 
+# (history per term, params, interface jumps, field errors)
+TOL = {"simt": (1e-2, 1e-4, 1e-2, 1e-4), None: (1e-1, 1e-3, 1e-1, 1e-3)}
 
 
 @pytest.fixture(scope="module")
