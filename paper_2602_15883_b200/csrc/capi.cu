@@ -709,10 +709,10 @@ extern "C" int fr_jet_fwd(const fr_plan* p, const void* kparams, const void* pts
 }
 
 // ---------------------------------------------------------------------------
-// 32 parameters x 8 row groups per block: coalesced 256-byte row reads, the 8
+// 32 parameters x 16 row groups per block: coalesced 256-byte row reads, the 16
 // partial sums combined in a fixed order, then a fixed-order block sum of g^2
 // for the optimiser's global norm.
-constexpr int RG_P = 32, RG_R = 8;
+constexpr int RG_P = 32, RG_R = 16;  // 16 row groups: short dependent chains over the ~148 partial rows
 __global__ void __launch_bounds__(RG_P * RG_R) reduce_grad_kernel(const double* __restrict__ gpart, int rows, int np_pad,
                                                                   const int* __restrict__ map, int n, double* grad,
                                                                   int accumulate, double* norm_parts) {
@@ -787,6 +787,25 @@ __device__ double block_sum_fixed(double v, double* red) {
   return r;
 }
 
+// N independent values through the same fixed-shape tree at once (one barrier
+// per level for all of them): bit-identical to N block_sum_fixed calls
+template <int N>
+__device__ void block_sum_fixed_n(double (&v)[N], double* red /* N * ADAM_NT */) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) red[k * ADAM_NT + threadIdx.x] = v[k];
+  __syncthreads();
+  for (int w = ADAM_NT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        red[k * ADAM_NT + threadIdx.x] = __dadd_rn(red[k * ADAM_NT + threadIdx.x], red[k * ADAM_NT + threadIdx.x + w]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = red[k * ADAM_NT];
+  __syncthreads();
+}
+
 // One block per segment, the same strided partial sums + fixed tree as the
 // optimiser kernel's loss reduction below, so `sums` equals the history row's
 // parts bit for bit (and the wide path's tens of thousands of tile rows reduce
@@ -830,7 +849,7 @@ extern "C" int fr_reduce_loss(const double* lpart, const int* seg_rows_host, int
 template <typename T>
 __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, const int* __restrict__ map,
                                                        const int* __restrict__ mapT) {
-  __shared__ double red[ADAM_NT];
+  __shared__ double red9[9 * ADAM_NT];
   const int tid = threadIdx.x;
   const long long step0 = *a.step;  // steps taken so far
   const long long row = step0 - a.row_base;
@@ -842,12 +861,12 @@ __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, co
   } else {
     for (int i = tid; i < n; i += ADAM_NT) acc = __dadd_rn(acc, __dmul_rn(a.grad[i], a.grad[i]));
   }
-  const double norm = sqrt(block_sum_fixed(acc, red));
-
-  // ---- loss parts, history row, finiteness (objective.py:183-198) ----
-  bool skip = false;
+  // the norm and the 8 loss sums share one pass of the fixed tree (identical
+  // per-value order to separate trees: the history row still equals
+  // fr_reduce_loss's sums bit for bit)
+  double vals[9];
+  vals[0] = acc;
   if (a.lpart) {
-    double sums[8];
     int r0 = 0;
     for (int sgi = 0; sgi < 4; ++sgi) {
       double x = 0.0, y = 0.0;
@@ -855,10 +874,23 @@ __global__ void __launch_bounds__(ADAM_NT) adam_kernel(fr_adam_args a, int n, co
         x += a.lpart[2 * r];
         y += a.lpart[2 * r + 1];
       }
-      sums[2 * sgi] = block_sum_fixed(x, red);
-      sums[2 * sgi + 1] = block_sum_fixed(y, red);
+      vals[1 + 2 * sgi] = x;
+      vals[2 + 2 * sgi] = y;
       r0 += a.seg_rows[sgi];
     }
+  } else {
+#pragma unroll
+    for (int k = 1; k < 9; ++k) vals[k] = 0.0;
+  }
+  block_sum_fixed_n<9>(vals, red9);
+  const double norm = sqrt(vals[0]);
+
+  // ---- loss parts, history row, finiteness (objective.py:183-198) ----
+  bool skip = false;
+  if (a.lpart) {
+    double sums[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sums[k] = vals[1 + k];
     const double obs = a.n_obs > 0 ? sums[0] / a.n_obs : 0.0;
     const double pde = sums[2] / a.n_colloc;
     const double gu = a.n_ghost_total > 0 ? (sums[4] + sums[6]) / a.n_ghost_total : 0.0;
