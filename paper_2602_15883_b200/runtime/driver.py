@@ -384,6 +384,14 @@ class FrNcclTransport:
             self.comm = C.c_void_p()
 
 
+def _peer_access_everywhere(n_ranks):
+    """True when every visible GPU pair used by an n_ranks job (one per GPU,
+    or all ranks on one GPU) can access each other's memory."""
+    n_dev = torch.cuda.device_count()
+    devs = range(min(n_dev, n_ranks))
+    return all(a == b or torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs)
+
+
 class DistributedTrainer:
     """This process's rank of a torch.distributed group (one process per GPU).
 
@@ -427,6 +435,13 @@ class DistributedTrainer:
         self.graphs = {}
         self.launches_per_epoch = {}  # library kernels in each captured epoch graph
         self._ran_eager = False
+        if transport == "ipc" and not _peer_access_everywhere(plan.n_ranks):
+            # the peer-memory transport needs every pair of this node's GPUs to
+            # reach each other's memory (NVLink / NVSwitch); otherwise NCCL P2P
+            import warnings
+
+            warnings.warn("GPUs without peer access: the ghost exchange falls back to NCCL point-to-point")
+            transport = self.transport = "torch"
         if transport == "ipc":
             self._init_ipc(plan, ws, dtype, epochs, exchange_timeout)
             return

@@ -218,3 +218,25 @@ def test_device_uniform_host_view_is_the_reference_sample():
         assert np.array_equal(np.asarray(d), host.datasets[r].colloc_points)
         for ga, gb in zip(lazy.datasets[r].ghosts, host.datasets[r].ghosts):
             assert np.array_equal(ga.points, gb.points)  # ghosts: their own stream (tag 2)
+
+
+def test_reference_arm_json_contract():
+    """`bench.py --impl reference` runs the unmodified reference on the CPU
+    (tiny N_pde here) and prints the contract's JSON line: impl, unsampled
+    cpu_baseline, e2e, and the P = 1/2/4/8 process-backend scaling column."""
+    import json
+    import subprocess
+    import sys
+
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "flowrec")):
+        pytest.skip("reference not installed under baseline/_ref")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--n-pde", "4000",
+                        "--steps", "1", "--warmup", "0", "--cpu-scaling-epochs", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["unit"] == "colloc_pts/s" and line["value"] > 0
+    assert line["config"]["colloc_per_rank"] == 4000 and "unsampled" in line["cpu_baseline"]["sample"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
+    assert sorted(line["cpu_scaling"]["P"], key=int) == ["1", "2", "4", "8"]
+    assert line["cpu_scaling"]["P"]["1"]["strong_scaling_eff"] == 1.0
