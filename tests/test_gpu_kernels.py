@@ -208,6 +208,7 @@ def test_tf32_pde_loss_and_gradient(golden, i):
     assert plan.info.math == 1
     sq, g = engine.pde_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], float(meta[3]))
     ref_sq = float(golden[f"{t}/sq_pde"])
+    report(f"tf32_pde/{t}", loss=abs(sq - ref_sq) / abs(ref_sq), grad=rel_l2(g, golden[f"{t}/grad_pde"]))
     assert abs(sq - ref_sq) <= TF32_LOSS * abs(ref_sq), (sq, ref_sq)
     assert rel_l2(g, golden[f"{t}/grad_pde"]) < TF32_GRAD
 
@@ -221,6 +222,8 @@ def test_tf32_mse_loss_and_gradient(golden, i):
     plan = engine.get_plan(cfg, kind, re, "float32", math="tf32")
     su, sp, g = engine.mse_loss_grad(plan, golden[f"{t}/params"], golden[f"{t}/pts"], golden[f"{t}/tu"],
                                      golden[f"{t}/tp"], list(meta[6 : 6 + nv]), float(meta[4]), float(meta[5]))
+    report(f"tf32_mse/{t}", sq_u=abs(su - float(golden[f"{t}/sq_u"])) / abs(su),
+           sq_p=abs(sp - float(golden[f"{t}/sq_p"])) / abs(sp), grad=rel_l2(g, golden[f"{t}/grad_mse"]))
     assert abs(su - float(golden[f"{t}/sq_u"])) <= TF32_LOSS * abs(su)
     assert abs(sp - float(golden[f"{t}/sq_p"])) <= TF32_LOSS * abs(sp)
     assert rel_l2(g, golden[f"{t}/grad_mse"]) < TF32_GRAD
