@@ -192,6 +192,20 @@ class LocalTrainer:
         self.graphs = {}
         self._ran_eager = False
 
+    def close(self):
+        """Free the peer transport's blocks (after the device is idle)."""
+        if self.blocks:
+            torch.cuda.synchronize()
+            for b in self.blocks.values():
+                b.free()
+            self.blocks = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def enqueue_exchange(self):
         for r in self.order:
             self.workers[r].produce()
@@ -530,7 +544,9 @@ class DistributedTrainer:
             self._ran_eager = True
 
     def close(self):
-        """Unmap the peers' blocks (IPC) / destroy the library's communicator."""
+        """Unmap the peers' blocks (IPC) / destroy the library's communicator.
+        This rank's own block is freed by `free()`, once every peer has closed
+        (a barrier between the two on every rank)."""
         from .. import _lib as X
 
         for ptr in getattr(self, "peer_ptrs", {}).values():
@@ -538,6 +554,12 @@ class DistributedTrainer:
         self.peer_ptrs = {}
         if getattr(self, "_post", None) is not None and hasattr(self._post, "close"):
             self._post.close()
+
+    def free(self):
+        blk = getattr(self, "block", None)
+        if blk is not None:
+            torch.cuda.synchronize()
+            blk.free()
 
     def _du(self, k):
         b = self.send_bufs[k]
@@ -613,6 +635,8 @@ def _train_distributed(plan, dtype, exchange_timeout=600.0, transport="ipc"):
     dist.all_gather_object(exports, (tr.rank, tr.worker.export()))
     dist.barrier()  # no peer may unmap / free a block another rank still stores into
     tr.close()
+    dist.barrier()  # every peer has unmapped this rank's block
+    tr.free()
     return _collect(plan, dict(exports), time.perf_counter() - t0)
 
 

@@ -163,5 +163,6 @@ def test_distributed_trainer_ipc_world1(golden):
         ref.workers[0].sync_history()
         assert np.array_equal(np.array(tr.worker.history)[:, 1:], np.array(ref.workers[0].history)[:, 1:])
         tr.close()
+        tr.free()
     finally:
         dist.destroy_process_group()
