@@ -50,7 +50,7 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   if (!attrs) {
     cudaFuncSetAttribute(tcw_fwd_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
     cudaFuncSetAttribute(tcw_fwdp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(float) * TCP_NS * C::stage_floats(256)));
+                         int(sizeof(float) * TCP_NS * C::fwdp_stage_floats(256)));
     cudaFuncSetAttribute(tcw_dx_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
     cudaFuncSetAttribute(tcw_dxp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(tcp_dx_smem<C>(256)));
@@ -62,7 +62,7 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   if (tc_persistent_fwd()) {
     const long long items = (long long)a.ntiles * (a.WP / NB);
     const int grid = int(std::min<long long>(items, tc_num_sms()));
-    const size_t smem = sizeof(float) * TCP_NS * C::stage_floats(NB);
+    const size_t smem = sizeof(float) * TCP_NS * C::fwdp_stage_floats(NB);
     for (int l = 1; l < a.L; ++l) tcw_fwdp_kernel<ACT, MODE, REG><<<grid, TCP_FWD_NT, smem, st>>>(a, l);
   } else {
     for (int l = 1; l < a.L; ++l) tcw_fwd_kernel<ACT, MODE, REG><<<gt, TC_FWD_NT, C::gemm_smem(NB), st>>>(a, l);

@@ -51,6 +51,33 @@ struct TcCfg {
   static constexpr int TPP = ITEMS <= NT ? 4 : 1;  // threads holding partial sums of one point (head)
   __host__ __device__ static constexpr int row0(int pt) { return (pt / PPW) * 32 + (pt % PPW) * S; }
   __host__ __device__ static constexpr size_t stage_floats(int NB) { return 2048 + size_t(NB) * 16; }
+  // persistent forward: the activation slab's unit quads are FQS floats apart
+  // (128 rows x 4 + 4): quad q shifts every row by 4 banks, which makes the St
+  // row-quad gather conflict-free and, with fwd_item(), the jet activation's
+  // 16-byte loads / stores nearly so (tools/bank_model.py)
+  static constexpr int FQS = 516;
+  __host__ __device__ static constexpr size_t fwdp_stage_floats(int NB) { return 4 * FQS + size_t(NB) * 16; }
+  // (point, unit quad) of activation item i: each 8-lane phase takes 4 points of
+  // one 32-row group x 2 quads, whose 16-byte rows then fall in 8 distinct
+  // bank groups (rows 6p mod 8 = {0,6,4,2}, quads +1); the 4th point of every
+  // group (rows 24..29, residue 0) fills the last two phases
+  static constexpr bool FWD_MAP = (PPW == 5 && PPT == 20 && ITEMS == 80);
+  __device__ static void fwd_item(int i, int& pt, int& kq) {
+    if constexpr (FWD_MAP) {
+      if (i < 64) {
+        const int ph = i >> 3, p8 = i & 7;
+        pt = 5 * (ph >> 1) + (p8 >> 1);
+        kq = 2 * (ph & 1) + (p8 & 1);
+      } else {
+        const int j = i - 64, p8 = j & 7;
+        pt = 5 * (2 * (j >> 3) + (p8 >> 2)) + 4;
+        kq = p8 & 3;
+      }
+    } else {
+      pt = i % PPT;
+      kq = i / PPT;
+    }
+  }
   __host__ __device__ static size_t gemm_smem(int NB) { return sizeof(float) * TC_NS * stage_floats(NB); }
   __host__ __device__ static size_t dw_stage_bytes(int WP, int NB) { return size_t(WP + NB) * 128; }
   static constexpr int HEAD_RED = PPT * 16 * NOUT;  // [pt][kq][j][o]
@@ -116,15 +143,15 @@ struct TcUnit {
   static constexpr bool ON = 2 * C::ITEMS <= 128 || (ADJ && ACT == ACT_SIN && (C::ITEMS % 128) != 0);
   static constexpr int N = ON ? C::ITEMS * 4 : C::ITEMS;
 };
-template <class C>
+template <class C, int QS = 512>
 __device__ __forceinline__ void slab_load1(float (&v)[C::S], const float* slab, int pt, int kq, int j) {
-  const float* b = slab + kq * 512 + C::row0(pt) * 4 + j;
+  const float* b = slab + kq * QS + C::row0(pt) * 4 + j;
 #pragma unroll
   for (int s = 0; s < C::S; ++s) v[s] = b[4 * s];
 }
-template <class C>
+template <class C, int QS = 512>
 __device__ __forceinline__ void slab_store1(float* slab, int pt, int kq, int j, const float (&v)[C::S]) {
-  float* b = slab + kq * 512 + C::row0(pt) * 4 + j;
+  float* b = slab + kq * QS + C::row0(pt) * 4 + j;
 #pragma unroll
   for (int s = 0; s < C::S; ++s) b[4 * s] = v[s];
 }
@@ -191,15 +218,15 @@ __device__ __forceinline__ void tc_act_bwd1(const float (&z)[C::S], float (&sb)[
 }
 
 // the S rows x 4 units of item (pt, kq) in a [kq][128][4] slab
-template <class C>
+template <class C, int QS = 512>
 __device__ __forceinline__ void slab_load(float (&v)[C::S][4], const float* slab, int pt, int kq) {
-  const float* b = slab + kq * 512 + C::row0(pt) * 4;
+  const float* b = slab + kq * QS + C::row0(pt) * 4;
 #pragma unroll
   for (int s = 0; s < C::S; ++s) vload(v[s], b + 4 * s);
 }
-template <class C>
+template <class C, int QS = 512>
 __device__ __forceinline__ void slab_store(float* slab, int pt, int kq, const float (&v)[C::S][4]) {
-  float* b = slab + kq * 512 + C::row0(pt) * 4;
+  float* b = slab + kq * QS + C::row0(pt) * 4;
 #pragma unroll
   for (int s = 0; s < C::S; ++s) vstore(b + 4 * s, v[s]);
 }
@@ -218,13 +245,13 @@ __device__ __forceinline__ size_t tc_toff(const WArgs& a, int l, long long tile)
 // its unit's 4 rows with scalar shared loads and writes one 16-byte store, so
 // 16 lanes cover a contiguous 256-byte run.  Pad rows are written as zeros so
 // they contribute nothing to the weight gradients.
-template <class C>
+template <class C, int QS = 512>
 __device__ __forceinline__ void slab_store_t(const float* slab, float* dstT, int WP, int k0, int tid) {
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     const int item = it * 128 + tid;
     const int rq = item >> 4, k16 = item & 15;
-    const float* src = slab + (k16 >> 2) * 512 + (4 * rq) * 4 + (k16 & 3);
+    const float* src = slab + (k16 >> 2) * QS + (4 * rq) * 4 + (k16 & 3);
     float v[4];
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
@@ -234,11 +261,13 @@ __device__ __forceinline__ void slab_store_t(const float* slab, float* dstT, int
     *reinterpret_cast<float4*>(dstT + (size_t(rq) * WP + k0 + k16) * 4) = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
-// plain copy of a [4 kq][128][4] slab to its (contiguous 8 KB) place in HBM
+// plain copy of a [4 kq][128][4] slab (quads QS floats apart) to its
+// (contiguous 8 KB) place in HBM
+template <int QS = 512>
 __device__ __forceinline__ void slab_copy_out(const float* slab, float* dst, int tid) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    reinterpret_cast<float4*>(dst)[tid + 128 * i] = reinterpret_cast<const float4*>(slab)[tid + 128 * i];
+    reinterpret_cast<float4*>(dst + 512 * i)[tid] = reinterpret_cast<const float4*>(slab + QS * i)[tid];
 }
 
 // 2 K-steps (16 deep) of A[kq][MA][4] x B[kq][NB][4]
@@ -412,7 +441,8 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
   const uint32_t tmem = tc_setup<512>(&tslot, mmad, TCP_NS);
   const int nch = a.WP / TC_KC;
   const bool virt = (l == 1);
-  const size_t SF = C::stage_floats(NB);
+  constexpr int QS = C::FQS;
+  const size_t SF = C::fwdp_stage_floats(NB);
   auto arrive = [&](uint64_t* bar) {
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
@@ -433,8 +463,9 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
           }
           float* st = ring + s * SF;
           tc::mbar_expect_tx(&full[s], NB * 64 + (virt ? 0 : 8192));
-          tc::bulk_g2s(st + 2048, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
-          if (!virt) tc::bulk_g2s(st, zsrc + size_t(c) * 2048, 8192, &full[s]);
+          tc::bulk_g2s(st + 4 * QS, tc_wslab(a, a.tcw_f, l, nb, c), NB * 64, &full[s]);
+          if (!virt)
+            for (int q = 0; q < 4; ++q) tc::bulk_g2s(st + q * QS, zsrc + size_t(c) * 2048 + q * 512, 2048, &full[s]);
         }
       }
     }
@@ -453,7 +484,11 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
           float* A = ring + s * SF;
           tc::mbar_wait(&actd[s], uint32_t(g / TCP_NS) & 1);
           tc::fence_after();
-          tc_mma16(tmem + b * 256, A, 128, A + 2048, NB, idesc, c == 0);
+          // 2 K-steps (16 deep): A quads QS floats apart (LBO), B = the NB x 16 weight slab
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            tc::mma_tf32(tmem + b * 256, tc::desc(A + kk * 2 * QS, QS * 4, 128),
+                         tc::desc(A + 4 * QS + kk * 8 * NB, NB * 16, 128), idesc, (c != 0 || kk) ? 1u : 0u);
           tc::mma_commit(&mmad[s]);
         }
         tc::mma_commit(&accf[b]);
@@ -468,7 +503,7 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = int(g % TCP_NS);
         tc::mbar_wait(&actd[s], uint32_t(g / TCP_NS) & 1);
-        if (st0) slab_store_t<C>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
+        if (st0) slab_store_t<C, QS>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
         arrive(&std_[s]);
       }
     }
@@ -513,16 +548,17 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
             const int j = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
             float z[C::S], sv[C::S];
             if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, 16 * c + 4 * kq + j, z);
-            else slab_load1<C>(z, A, pt, kq, j);
+            else slab_load1<C, QS>(z, A, pt, kq, j);
             tc_act1<C, ACT>(z, sv);
-            slab_store1<C>(A, pt, kq, j, sv);
+            slab_store1<C, QS>(A, pt, kq, j, sv);
           }
         } else
         for (int i = t; i < C::ITEMS; i += 128) {
-          const int pt = i % C::PPT, kq = i / C::PPT;
+          int pt, kq;
+          C::fwd_item(i, pt, kq);
           float z[C::S][4], sv[C::S][4];
           if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, 4 * c + kq, z);
-          else slab_load<C>(z, A, pt, kq);
+          else slab_load<C, QS>(z, A, pt, kq);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float zz[C::S], ss[C::S];
@@ -531,7 +567,7 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
 #pragma unroll
             for (int k = 0; k < C::S; ++k) sv[k][j] = ss[k];
           }
-          slab_store<C>(A, pt, kq, sv);
+          slab_store<C, QS>(A, pt, kq, sv);
         }
         tc::fence_proxy_async();
         arrive(&actd[s]);
@@ -725,7 +761,10 @@ constexpr int TCP_DX_NS = 4;
 constexpr int TCP_DX_NT = 576;
 template <class C>
 __host__ __device__ constexpr int tcp_dx_epi() {  // floats of one epilogue group's buffers
-  return 4 * 2048 > 2048 + C::PPT * 16 * (C::DIN + 1) ? 4 * 2048 : 2048 + C::PPT * 16 * (C::DIN + 1);
+  // stg[2] + zc[2] slabs with padded unit quads (C::FQS, see the forward), or
+  // (l == 1) stg[0] + the dW_0 reduction buffer
+  return 4 * 4 * C::FQS > 4 * C::FQS + C::PPT * 16 * (C::DIN + 1) ? 4 * 4 * C::FQS
+                                                                  : 4 * C::FQS + C::PPT * 16 * (C::DIN + 1);
 }
 template <class C>
 __host__ __device__ constexpr size_t tcp_dx_smem(int NB) {
@@ -763,9 +802,12 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   const bool virt = (l == 1);
   // epilogue group grp (items with it % 2 == grp, i.e. TMEM accumulator grp)
   const int grp = warp >= 10 ? 1 : 0, wl = warp - 10 * grp;
-  float* stg = ring + TCP_DX_NS * SF + grp * tcp_dx_epi<C>();  // [2][4][128][4]  S-bar / Zbar columns
-  float* zc = stg + 2 * 2048;          // [2][4][128][4]  Z_{l-1} slabs
-  float* red = stg + 2048;             // l == 1: [PPT][4 kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
+  // epilogue slabs: unit quads QS floats apart (conflict-free act-bwd items
+  // with fwd_item() and a conflict-free row-quad gather for Zbar^T)
+  constexpr int QS = C::FQS, QSL = 4 * QS;
+  float* stg = ring + TCP_DX_NS * SF + grp * tcp_dx_epi<C>();  // [2][4 kq (QS)][128][4]  S-bar / Zbar columns
+  float* zc = stg + 2 * QSL;          // [2][4 kq (QS)][128][4]  Z_{l-1} slabs
+  float* red = stg + QSL;             // l == 1: [PPT][4 kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
   uint64_t* zfull = zfull_[grp];
   uint64_t* rdy = rdy_[grp];
   uint64_t* done = done_[grp];
@@ -826,7 +868,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
       }
       if (w >= nitems) return;
       tc::mbar_expect_tx(&zfull[b], 8192);
-      tc::bulk_g2s(zc + b * 2048, zslab(w, j), 8192, &zfull[b]);
+      for (int q = 0; q < 4; ++q) tc::bulk_g2s(zc + b * QSL + q * QS, zslab(w, j) + q * 512, 2048, &zfull[b]);
     };
     const long long w0 = blockIdx.x + (long long)grp * gridDim.x;
     if (!virt && et == 0 && w0 < nitems)
@@ -839,14 +881,14 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
       tc::fence_after();
       for (int j = 0; j < nck; ++j, ++jg) {
         const int b = virt ? 0 : int(jg & 1);
-        float* sg = stg + b * 2048;
+        float* sg = stg + b * QSL;
         if (!virt && jg >= 2) tc::mbar_wait(&done[b], uint32_t((jg - 2) >> 1) & 1);
         {
           float v[16];
           tc::tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + ab * 256 + 16 * j, v);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(sg + q * 512 + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            *reinterpret_cast<float4*>(sg + q * QS + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
         if (j == nck - 1) {
           tc::fence_before();
@@ -854,17 +896,19 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         }
         sync_e();
         if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
-        const float* zs = zc + b * 2048;
+        const float* zs = zc + b * QSL;
         if constexpr (TcUnit<C, true, ACT>::ON) {
           for (int i = et; i < TcUnit<C, true, ACT>::N; i += 128) {
-            const int jj = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
+            const int jj = i & 3;
+            int pt, kq;
+            C::fwd_item(i >> 2, pt, kq);
             float z[C::S], sb[C::S], sa[C::S];
             if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 16 * j + 4 * kq + jj, z);
-            else slab_load1<C>(z, zs, pt, kq, jj);
-            slab_load1<C>(sb, sg, pt, kq, jj);
+            else slab_load1<C, QS>(z, zs, pt, kq, jj);
+            slab_load1<C, QS>(sb, sg, pt, kq, jj);
             tc_act_bwd1<C, ACT>(z, sb, sa);
             if (!virt) {
-              slab_store1<C>(sg, pt, kq, jj, sb);  // Zbar_{l-1}, in place of S-bar
+              slab_store1<C, QS>(sg, pt, kq, jj, sb);  // Zbar_{l-1}, in place of S-bar
             } else {
               const long long p = tile * C::PPT + pt;
               const bool live = p < a.n;
@@ -881,12 +925,13 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
           }
         } else
         for (int i = et; i < C::ITEMS; i += 128) {
-          const int pt = i % C::PPT, kq = i / C::PPT;
+          int pt, kq;
+          C::fwd_item(i, pt, kq);
           const int q = n0 / 4 + 4 * j + kq;
           float z[C::S][4], sb[C::S][4];
           if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
-          else slab_load<C>(z, zs, pt, kq);
-          slab_load<C>(sb, sg, pt, kq);
+          else slab_load<C, QS>(z, zs, pt, kq);
+          slab_load<C, QS>(sb, sg, pt, kq);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             float zz[C::S], bb[C::S], sa[C::S];
@@ -897,7 +942,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
             for (int k = 0; k < C::S; ++k) sb[k][jj] = bb[k];
           }
           if (!virt) {
-            slab_store<C>(sg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
+            slab_store<C, QS>(sg, pt, kq, sb);  // Zbar_{l-1}, in place of S-bar
           } else {
             const long long p = tile * C::PPT + pt;
             const bool live = p < a.n;
@@ -943,9 +988,9 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
       for (int j = 0; j < nck; ++j, ++jg) {
         const int b = int(jg & 1);
         tc::mbar_wait(&rdy[b], uint32_t(jg >> 1) & 1);
-        const float* sg = stg + b * 2048;
-        slab_copy_out(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
-        slab_store_t<C>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+        const float* sg = stg + b * QSL;
+        slab_copy_out<QS>(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
+        slab_store_t<C, QS>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
         arrive(&done[b]);
       }
     }
