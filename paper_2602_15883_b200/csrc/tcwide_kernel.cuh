@@ -78,12 +78,24 @@ struct TcCfg {
       kq = i / PPT;
     }
   }
+  // inverse of fwd_item: the item index that holds (pt, kq)
+  __device__ static int item_of(int pt, int kq) {
+    if constexpr (FWD_MAP) {
+      const int g = pt / 5, p = pt % 5;
+      return p < 4 ? 8 * (2 * g + (kq >> 1)) + 2 * p + (kq & 1) : 64 + 8 * (g >> 1) + 4 * (g & 1) + kq;
+    } else {
+      return kq * PPT + pt;
+    }
+  }
   __host__ __device__ static size_t gemm_smem(int NB) { return sizeof(float) * TC_NS * stage_floats(NB); }
   __host__ __device__ static size_t dw_stage_bytes(int WP, int NB) { return size_t(WP + NB) * 128; }
-  static constexpr int HEAD_RED = PPT * 16 * NOUT;  // [pt][kq][j][o]
+  // head dW_L partials: [pt][kq][j][o] for per-unit items, else [j][o][item]
+  // rows of HRS = ITEMS + 1 floats (lane-contiguous stores, odd row stride)
+  static constexpr int HRS = ITEMS + 1;
+  static constexpr int HEAD_RED = 4 * NOUT * HRS;
   __host__ __device__ static size_t head_smem(int WP) {
     return sizeof(double) * 2 * NT +
-           sizeof(float) * size_t(TC_NS * 2048 + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
+           sizeof(float) * size_t(TC_NS * 4 * FQS + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
   }
 };
 
@@ -1129,12 +1141,13 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   static_assert(!HU || (NT % (4 * PPT) == 0 && 4 * C::ITEMS % NT == 0), "per-unit head split");
   extern __shared__ __align__(128) unsigned char tc_smem[];
   double* lred = reinterpret_cast<double*>(tc_smem);      // [2][NT]
-  float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][2048]
-  float* WLs = ring + TC_NS * 2048;                        // [WP][NOUT]
+  constexpr int QS = C::FQS, SF = 4 * QS;                 // padded unit quads (see TcCfg::FQS)
+  float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][4][QS]
+  float* WLs = ring + TC_NS * SF;                          // [WP][NOUT]
   float* Yp = WLs + a.WP * NOUT;                           // [NT][SN]
   float* Ys = Yp + NT * SN;                                // [PPT][SN]
   float* Ybs = Ys + PPT * SN;                              // [PPT][SN]
-  float* red = Ybs + PPT * SN;                             // [PPT][4][4][NOUT]
+  float* red = Ybs + PPT * SN;                             // see TcCfg::HEAD_RED
   __shared__ __align__(8) uint64_t full[TC_NS];
   const long long tile = blockIdx.x;
   const int tid = threadIdx.x;
@@ -1150,7 +1163,9 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   auto produce = [&](int g) {
     const int s = g % TC_NS;
     tc::mbar_expect_tx(&full[s], 8192);
-    tc::bulk_g2s(ring + s * 2048, zsrc + size_t(g % nch) * 2048, 8192, &full[s]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      tc::bulk_g2s(ring + s * SF + q * QS, zsrc + size_t(g % nch) * 2048 + q * 512, 2048, &full[s]);
   };
   if (tid == 0)
     for (int g = 0; g < TC_NS && g < ntot; ++g) produce(g);
@@ -1170,7 +1185,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
         const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
         float zz[S], ss[S];
-        slab_load1<C>(zz, ring + s * 2048, pt, kq, j);
+        slab_load1<C, QS>(zz, ring + s * SF, pt, kq, j);
         tc_act1<C, ACT>(zz, ss);
         const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
 #pragma unroll
@@ -1180,9 +1195,10 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       }
     } else
     for (int i = tid; i < C::ITEMS; i += NT) {
-      const int pt = i % PPT, kq = i / PPT;
+      int pt, kq;
+      C::fwd_item(i, pt, kq);
       float z[S][4];
-      slab_load<C>(z, ring + s * 2048, pt, kq);
+      slab_load<C, QS>(z, ring + s * SF, pt, kq);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float zz[S], ss[S];
@@ -1211,7 +1227,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     float* yb = Ybs + pt * SN;
     for (int i = 0; i < SN; ++i) {
       float v = 0.f;
-      for (int h = 0; h < TPPH; ++h) v += Yp[(HU ? 4 * (pt + PPT * (h >> 2)) + (h & 3) : pt + PPT * h) * SN + i];
+      for (int h = 0; h < TPPH; ++h) v += Yp[(HU ? 4 * (pt + PPT * (h >> 2)) + (h & 3) : C::item_of(pt, h)) * SN + i];
       yv[i] = (i < NOUT) ? v + kp[pl.off_b(L) + i] : v;
       yb[i] = 0.f;
     }
@@ -1299,15 +1315,17 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   // ---- adjoint: S-bar = Ybar W_L^T, act-bwd, dW_L partial ----
   for (int c = 0; c < nch; ++c) {
     const int g = nch + c, s = g % TC_NS;
-    float* slab = ring + s * 2048;
+    float* slab = ring + s * SF;
     tc::mbar_wait(&full[s], (g / TC_NS) & 1);
     if constexpr (HU) {
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
         const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
-        const float* yb = Ybs + pt * SN;
+        float yb[SN];  // registers: the red / slab stores below may alias Ybs
+#pragma unroll
+        for (int e = 0; e < SN; ++e) yb[e] = Ybs[pt * SN + e];
         const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
         float zz[S], bb[S], sa[S];
-        slab_load1<C>(zz, slab, pt, kq, j);
+        slab_load1<C, QS>(zz, slab, pt, kq, j);
 #pragma unroll
         for (int st = 0; st < S; ++st) {
           float v = 0.f;
@@ -1324,15 +1342,18 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
           for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
           rd[o] = v;
         }
-        slab_store1<C>(slab, pt, kq, j, bb);  // Zbar_{L-1} in place of Z_{L-1}
+        slab_store1<C, QS>(slab, pt, kq, j, bb);  // Zbar_{L-1} in place of Z_{L-1}
       }
     } else
     for (int i = tid; i < C::ITEMS; i += NT) {
-      const int pt = i % PPT, kq = i / PPT;
+      int pt, kq;
+      C::fwd_item(i, pt, kq);
       const int q = 4 * c + kq;
-      const float* yb = Ybs + pt * SN;
+      float yb[SN];  // registers: the red / slab stores below may alias Ybs
+#pragma unroll
+      for (int e = 0; e < SN; ++e) yb[e] = Ybs[pt * SN + e];
       float z[S][4], sb[S][4];
-      slab_load<C>(z, slab, pt, kq);
+      slab_load<C, QS>(z, slab, pt, kq);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float* w = WLs + (4 * q + j) * NOUT;
@@ -1348,24 +1369,25 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
         tc_act_bwd1<C, ACT>(zz, bb, sa);
 #pragma unroll
         for (int st = 0; st < S; ++st) sb[st][j] = bb[st];
-        float* rd = red + ((pt * 4 + kq) * 4 + j) * NOUT;
+        float* rd = red + j * NOUT * C::HRS + i;
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) {
           float v = 0.f;
 #pragma unroll
           for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
-          rd[o] = v;
+          rd[o * C::HRS] = v;
         }
       }
-      slab_store<C>(slab, pt, kq, sb);  // Zbar_{L-1} in place of Z_{L-1}
+      slab_store<C, QS>(slab, pt, kq, sb);  // Zbar_{L-1} in place of Z_{L-1}
     }
     __syncthreads();
-    slab_copy_out(slab, static_cast<float*>(a.adj) + tc_off(a, L - 1, tile, 4 * c), tid);
-    slab_store_t<C>(slab, a.zt + tc_toff(a, L - 1, tile), a.WP, 16 * c, tid);
+    slab_copy_out<QS>(slab, static_cast<float*>(a.adj) + tc_off(a, L - 1, tile, 4 * c), tid);
+    slab_store_t<C, QS>(slab, a.zt + tc_toff(a, L - 1, tile), a.WP, 16 * c, tid);
     for (int e = tid; e < 16 * NOUT; e += NT) {
       const int kq = e / (4 * NOUT), j = (e / NOUT) % 4, o = e % NOUT;
       float acc = 0.f;
-      for (int pt = 0; pt < PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + j) * NOUT + o];
+      for (int pt = 0; pt < PPT; ++pt)
+        acc += HU ? red[((pt * 4 + kq) * 4 + j) * NOUT + o] : red[(j * NOUT + o) * C::HRS + C::item_of(pt, kq)];
       pL[size_t(16 * c + 4 * kq + j) * NOUT + o] = acc;
     }
     __syncthreads();
