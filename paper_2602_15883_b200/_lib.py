@@ -129,6 +129,7 @@ _SIGS = {
     "fr_bench_ffma": [C.c_int, C.c_int, C.c_int, _P, _P],
     "fr_debug_tc_gemm_tf32": [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P],
     "fr_debug_tc_raw": [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P],
+    "fr_debug_tc_raw2": [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P],
 }
 EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version", "fr_kernel_launches")
 

@@ -181,6 +181,7 @@ struct JetCfg {
     e += al(ROWS * NOUT);                  // Ys
     if (BWD) e += al(ROWS * NOUT);         // Ybs
     e += al(PPT * DIN);                    // Ps
+    if (tc) e += 256;                      // 1 KB: the base is aligned up for the MN-major dW atoms
     // (MSE targets are read from global in the head; the db partials alias Ys,
     // which is dead once the head has run)
     return e;
@@ -239,10 +240,12 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 #define FR_EPOCH_2CTA 0  // two 192-thread CTAs per SM: measured slower (5.89 vs 5.40 ms), kept as a tuning switch
 #endif
 #ifndef FR_TC_DW
-// tensor-core weight gradient (tc3_dw): correct, but with only the idle weight
-// slot (32 KB) to stage the transposed operands it runs 16-row chunks
-// double-buffered and is bound by the MMA -> commit round trip: measured 16.6k
-// vs 13.7k cycles per tile-layer for the SIMT dW, so off
+// tensor-core weight gradient (tc3_dw): MN-major BASE32B operands staged from
+// the k-quad buffers through the idle 32 KB weight slot.  Correct (grad ~1e-6),
+// but with one 32-row chunk buffer the staging copies, the per-chunk MMA
+// round trip and the TMEM drain cost as much as the SIMT FFMA2 dW they replace
+// (phase timers: 5.7k + 5.1k + 3.4k vs 13.7k cycles per tile-layer; 16-row
+// double-buffered chunks are slower still), so off.  DESIGN.md 4.
 #define FR_TC_DW 0
 #endif
 #ifndef FR_DW_SPLIT6
@@ -672,63 +675,84 @@ __device__ __forceinline__ void tc3_drain(float* out, TcState& t) {
 
 // Weight gradient of one hidden layer on the tensor core:
 //     dW[i][o] = sum_rows H[row][i] Zbar[row][o]
-// with K = rows.  TF32 operands must be K-major, i.e. rows contiguous -- the
-// transpose of the k-quad layout -- so the tile's rows are staged 16 at a time
-// into two 16 KB buffers (double-buffered against the MMAs):
-//     A = [H^T_hi ; H^T_lo]  (M = 128: in-units hi, then lo)   [4 row quads][128][4]
-//     B = [Zbar^T_hi ; Zbar^T_lo] (N = 128: out-units hi, then lo)
+// with K = rows, both operands MN-major (units contiguous).  sm_100a reads
+// MN-major TF32 only in the SWIZZLE_128B_BASE32B canonical layout (512-byte
+// atoms of 4 K rows x 32 MN elements, 32-byte chunks XOR-swizzled by the row;
+// LBO = MN-group stride, SBO = K-group stride -- tools/tc_mn_probe.py), and a
+// k-quad 16-byte piece (one row, 4 units) stays contiguous in it, so staging a
+// chunk of RC rows is one LDS.128 + two STS.128 (hi, lo) per piece:
+//     A = [H ; H_lo]   (M = 128: in-units hi, then lo)
+//     B = [Zb ; Zb_lo] (N = 128: out-units hi, then lo)
 // and ONE M = N = 128 MMA per 8 rows yields every split product at once:
 // D[i][o] = H_hi Z_hi, D[i][64 + o] = H_hi Z_lo, D[64 + i][o] = H_lo Z_hi (the
 // fourth quadrant, H_lo Z_lo, is dropped).  The accumulator lives in TMEM
 // columns [384, 512) for the whole tile; the three quadrants are summed in
 // FP32 and red.add-ed into the CTA's f64 gradient row once per tile.  (hi is
 // the raw FP32 value, which the tensor core reads truncated; lo =
-// rna_tf32(x - trunc(x)).)  `stg` is the idle weight slot (32 KB), `scratch`
-// 4096 floats (free once the chunks are staged).
+// rna_tf32(x - trunc(x)).)  `stg` is the idle weight slot (32 KB, 512-byte
+// aligned): NBUF chunk buffers of RC rows; `scratch` 4160 floats (free once
+// the chunks are staged).
+#ifndef FR_TC_DW_RC
+#define FR_TC_DW_RC 32
+#endif
+__device__ __forceinline__ int b32_at(int m, int k, int RC) {
+  return (((m >> 5) * (RC >> 2) + (k >> 2)) << 7) + ((k & 3) << 5) + (((((m & 31) >> 3) ^ k) & 3) << 3) + (m & 7);
+}
+// The dX hi passes of the same layer (A = dx_a, B = dx_b) are issued right
+// after the last chunk, so the weight-gradient MMAs never queue behind them.
 template <int ROWS, int RS4, int NT, int W>
 __device__ __forceinline__ void tc3_dw(const float* H, const float* Zb, float* stg, float* scratch, double* gp_w,
-                                       TcState& t, int issuer) {
-  static_assert(W == 64 && ROWS % 16 == 0, "tensor-core weight gradient: W = 64, 16-row chunks");
-  constexpr int NCH = ROWS / 16;
+                                       TcState& t, int issuer, const float* dx_a, const float* dx_b) {
+  constexpr int RC = (FR_TC_DW_RC == 32 && ROWS % 32 == 0) ? 32 : 16, NBUF = 32 / RC;  // 32 rows x {A, B} = 32 KB
+  static_assert(W == 64 && ROWS % RC == 0, "tensor-core weight gradient: W = 64, 16-row chunks");
+  constexpr int NCH = ROWS / RC, OPF = 128 * RC;  // floats per operand ([4 MN groups][RC / 4 K groups][128])
   constexpr uint32_t DCOL = 384;
   const int tid = threadIdx.x;
-  const uint32_t id = tc::idesc_tf32(128, 128);
+  const uint32_t id = tc::idesc_tf32(128, 128, 1, 1);
+  FR_TC_START;
 #pragma unroll 1
   for (int c = 0; c < NCH; ++c) {
-    const int b = c & 1;
-    float* buf = stg + 4096 * b;
-    if (c >= 2) {  // the chunk-(c-2) MMAs must be done with this buffer
+    const int b = c % NBUF;
+    float* buf = stg + 2 * OPF * b;
+    if (c >= NBUF) {  // the chunk-(c - NBUF) MMAs must be done with this buffer
       mbar_wait_bounded(t.mbar_dw + b, (t.dw_phase >> b) & 1u);
       t.dw_phase ^= 1u << b;
     }
-    const int r0 = 16 * c;
-    for (int it = tid; it < 512; it += NT) {
-      const int which = it >> 8, rq = (it >> 6) & 3, u = it & 63;
-      const float* src = which ? Zb : H;
-      const float* sp = src + (u >> 2) * RS4 + (r0 + 4 * rq) * 4 + (u & 3);
-      const float4 v = make_float4(sp[0], sp[4], sp[8], sp[12]);
-      float* dst = buf + 2048 * which + (rq * 128 + u) * 4;
-      *reinterpret_cast<float4*>(dst) = v;
-      *reinterpret_cast<float4*>(dst + 256) = make_float4(tf32_alo(v.x), tf32_alo(v.y), tf32_alo(v.z), tf32_alo(v.w));
+    FR_TC_MARK(13);
+    const int r0 = RC * c;
+    for (int it = tid; it < 2 * RC * 16; it += NT) {
+      const int which = it / (RC * 16), r = (it >> 4) % RC, q = it & 15;
+      const float4 v = *reinterpret_cast<const float4*>((which ? Zb : H) + q * RS4 + (r0 + r) * 4);
+      float* dst = buf + which * OPF;
+      *reinterpret_cast<float4*>(dst + b32_at(4 * q, r, RC)) = v;
+      *reinterpret_cast<float4*>(dst + b32_at(64 + 4 * q, r, RC)) =
+          make_float4(tf32_alo(v.x), tf32_alo(v.y), tf32_alo(v.z), tf32_alo(v.w));
     }
+    FR_TC_MARK(14);
     tc::fence_proxy_async();
     __syncthreads();
+    FR_TC_MARK(15);
     if (tid == issuer) {
       tc::fence_after();
-      const uint64_t a0 = tc::desc(buf, 2048, 128), b0 = tc::desc(buf + 2048, 2048, 128);
-      mma_tf32_lit(t.tmem + DCOL, a0, b0, id, c != 0);
-      mma_tf32_lit(t.tmem + DCOL, a0 + uint64_t(4096 >> 4), b0 + uint64_t(4096 >> 4), id, true);
+      const uint64_t a0 = tc::desc(buf, RC / 4 * 512, 512) | (uint64_t(1) << 61);
+      const uint64_t b0 = tc::desc(buf + OPF, RC / 4 * 512, 512) | (uint64_t(1) << 61);
+#pragma unroll
+      for (int ks = 0; ks < RC / 8; ++ks)
+        mma_tf32_lit(t.tmem + DCOL, a0 + uint64_t((1024 * ks) >> 4), b0 + uint64_t((1024 * ks) >> 4), id,
+                     c != 0 || ks != 0);
       tc::mma_commit(t.mbar_dw + b);
     }
   }
-  // the last two chunks' completions (the last covers every MMA before it)
+  tc3_issue_hi<ROWS, RS4>(dx_a, dx_b, t, issuer);
+  // the last NBUF chunks' completions (the last covers every MMA before it)
 #pragma unroll
-  for (int k = NCH >= 2 ? NCH - 2 : 0; k < NCH; ++k) {
-    const int b = k & 1;
+  for (int k = NCH >= NBUF ? NCH - NBUF : 0; k < NCH; ++k) {
+    const int b = k % NBUF;
     mbar_wait_bounded(t.mbar_dw + b, (t.dw_phase >> b) & 1u);
     t.dw_phase ^= 1u << b;
   }
   tc::fence_after();
+  FR_TC_MARK(13);
   // drain: lanes 64..127 (H_lo Z_hi) into shared memory [o][i] (stride 65:
   // conflict-free both ways), lanes 0..63 add H_hi Z_hi + H_hi Z_lo to it, then
   // every thread red.adds a coalesced run of the 64 x 64 block once
@@ -764,6 +788,7 @@ __device__ __forceinline__ void tc3_dw(const float* H, const float* Zb, float* s
     red_add(gp_w + e, double(scratch[o * 65 + i]));
   }
   __syncthreads();
+  FR_TC_MARK(9);
 }
 
 // A_lo of a whole k-quad buffer, out of place (dst may not alias src)
@@ -1359,8 +1384,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
         constexpr bool SLOT_PARTIALS = RSPLIT_DW * W * W > C::XELEMS;
         constexpr int DX_ISSUER = TC_DW ? NT - 32
                                   : (C::KT * C::KT * RSPLIT_DW < NT) ? C::KT * C::KT * RSPLIT_DW : 0;
-        constexpr bool DX_EARLY = TC && FR_TC_DX_EARLY && C::KT * C::KT * RSPLIT_DW < NT;
-        if constexpr (DX_EARLY)
+        constexpr bool DX_EARLY = TC && (TC_DW || (FR_TC_DX_EARLY && C::KT * C::KT * RSPLIT_DW < NT));
+        if constexpr (DX_EARLY && !TC_DW)
           tc3_issue_hi<ROWS, RS4>(reinterpret_cast<const float*>(Gs),
                                   reinterpret_cast<const float*>((ws & 1) ? slot1 : slot0), *tcs, DX_ISSUER);
         if constexpr (TC_DW) {
@@ -1368,7 +1393,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
           // slot (the next matrix is prefetched after it); db_l on the SIMT side
           tc3_dw<ROWS, RS4, NT, W>(reinterpret_cast<const float*>(Xs), reinterpret_cast<const float*>(Gs),
                                    reinterpret_cast<float*>((ws & 1) ? slot0 : slot1), reinterpret_cast<float*>(Xs),
-                                   gp + pl.off_w(l), *tcs, DX_ISSUER);
+                                   gp + pl.off_w(l), *tcs, DX_ISSUER, reinterpret_cast<const float*>(Gs),
+                                   reinterpret_cast<const float*>((ws & 1) ? slot1 : slot0));
           FR_MARK(8);
           {
             constexpr int NH = NT / W;
@@ -1699,14 +1725,20 @@ __global__ void __launch_bounds__(EpochCfg<T, ACT, REG, W>::NT, EpochCfg<T, ACT,
     __syncthreads();
     tcs = &st;
   }
+  unsigned char* smem = smem_raw;
+  if constexpr (TC) {  // 1 KB-aligned carve: the weight slots then start on 512-byte BASE32B atom boundaries
+    smem += (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+    static_assert(TC == false || (2 * JetCfg<T, ACT, MODE_PDE, REG, W, NT>::al(JetCfg<T, ACT, MODE_PDE, REG, W, NT>::XELEMS) * 4) % 512 == 0,
+                  "weight slots on 512-byte boundaries");
+  }
   double* gp = e.pde.gpart + size_t(c) * e.pde.np_pad;
   TcState local{};
   if constexpr (TC) local = *tcs;  // every thread tracks the barrier phase in a register
-  run_tiles<T, ACT, MODE_PDE, REG, W, NT, TC>(e.pde, smem_raw, c, G, true, gp, e.pde.lpart + 2 * c, &local);
+  run_tiles<T, ACT, MODE_PDE, REG, W, NT, TC>(e.pde, smem, c, G, true, gp, e.pde.lpart + 2 * c, &local);
   long long offset = (e.pde.n + JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_PDE, REG, W, NT>::PPT;
   for (int d = 0; d < e.n_mse; ++d) {
     const long long t0 = ((c - offset) % G + G) % G;
-    run_tiles<T, ACT, MODE_MSE, REG, W, NT, TC>(e.mse[d], smem_raw, t0, G, false, gp, e.mse[d].lpart + 2 * c,
+    run_tiles<T, ACT, MODE_MSE, REG, W, NT, TC>(e.mse[d], smem, t0, G, false, gp, e.mse[d].lpart + 2 * c,
                                                 &local);
     offset += (e.mse[d].n + JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT - 1) / JetCfg<T, ACT, MODE_MSE, REG, W, NT>::PPT;
   }

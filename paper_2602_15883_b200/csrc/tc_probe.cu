@@ -8,23 +8,32 @@
 namespace fr {
 
 // k-quad staging: X[(k>>2)*(rows*4) + row*4 + (k&3)]
-// layout bit 0: A MN-major, bit 1: B MN-major
+// layout bit 0: A MN-major, bit 1: B MN-major; bit 2: MN-major operands in the
+// SWIZZLE_128B_BASE32B canonical layout (512-byte atoms of 4 K rows x 32 MN
+// elements, 32-byte chunks XOR-swizzled by the row) instead of SWIZZLE_NONE;
+// bit 3: swap the LBO / SBO roles of the BASE32B descriptor
+__device__ __forceinline__ int b32_off(int mn, int k, int K) {
+  // atoms [mn / 32][k / 4], 128 floats each
+  const int atom = (mn >> 5) * (K >> 2) + (k >> 2), kr = k & 3, e = mn & 31;
+  return atom * 128 + kr * 32 + ((((e >> 3) ^ kr) & 3) << 3) + (e & 7);
+}
 __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                       float* __restrict__ C, int N, int K, int ncols, int layout) {
   extern __shared__ __align__(128) float sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tbase;
-  float* As = sm;
-  float* Bs = sm + 128 * K;
+  float* As = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
+  float* Bs = As + 128 * K;
+  const bool b32 = layout & 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 128 * K; i += 128) {
     const int r = i / K, k = i % K;
-    if (layout & 1) As[(r >> 2) * (K * 4) + k * 4 + (r & 3)] = A[i];
+    if (layout & 1) As[b32 ? b32_off(r, k, K) : (r >> 2) * (K * 4) + k * 4 + (r & 3)] = A[i];
     else As[(k >> 2) * 512 + r * 4 + (k & 3)] = A[i];
   }
   for (int i = tid; i < N * K; i += 128) {
     const int r = i / K, k = i % K;
-    if (layout & 2) Bs[(r >> 2) * (K * 4) + k * 4 + (r & 3)] = B[i];
+    if (layout & 2) Bs[b32 ? b32_off(r, k, K) : (r >> 2) * (K * 4) + k * 4 + (r & 3)] = B[i];
     else Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = B[i];
   }
   if (warp == 0) {
@@ -45,11 +54,18 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__
   const uint32_t tmem = tbase;
   if (tid == 0) {
     const uint32_t idesc = tc::idesc_tf32(128, N, layout & 1, (layout >> 1) & 1);
+    // BASE32B: MN-group (32 elements) stride K/4 atoms, K-group (4 rows) stride one 512-byte atom
+    const uint32_t mg = uint32_t(K / 4) * 512, kg = 512;
+    const uint32_t b_lbo = (layout & 8) ? kg : mg, b_sbo = (layout & 8) ? mg : kg;
     for (int kk = 0; kk < K / 8; ++kk) {
       // K-major: LBO = K-chunk stride, SBO = 8-row stride; MN-major: LBO = 8-k stride, SBO = 4-row group stride
-      const uint64_t ad = (layout & 1) ? tc::desc(As + kk * 32, 128, K * 16) : tc::desc(As + kk * 2 * 512, 512 * 4, 128);
-      const uint64_t bd = (layout & 2) ? tc::desc(Bs + kk * 32, 128, K * 16)
-                                       : tc::desc(Bs + kk * 2 * (N * 4), N * 16, 128);
+      uint64_t ad, bd;
+      if (!(layout & 1)) ad = tc::desc(As + kk * 2 * 512, 512 * 4, 128);
+      else if (b32) ad = tc::desc(As + kk * 256, b_lbo, b_sbo) | (uint64_t(1) << 61);
+      else ad = tc::desc(As + kk * 32, 128, K * 16);
+      if (!(layout & 2)) bd = tc::desc(Bs + kk * 2 * (N * 4), N * 16, 128);
+      else if (b32) bd = tc::desc(Bs + kk * 256, b_lbo, b_sbo) | (uint64_t(1) << 61);
+      else bd = tc::desc(Bs + kk * 32, 128, K * 16);
       tc::mma_tf32(tmem, ad, bd, idesc, kk > 0);
     }
     tc::mma_commit(&mbar);
@@ -77,7 +93,7 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(const float* __restrict__
 extern "C" int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K, int layout,
                                      fr_stream_t stream) {
   if (N < 16 || N > 256 || N % 16 || K < 8 || K % 8 || K > 64) return -1;
-  const size_t smem = sizeof(float) * size_t(128 + N) * K;
+  const size_t smem = sizeof(float) * size_t(128 + N) * K + 1024;
   if (cudaFuncSetAttribute(fr::tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess)
     return -2;
@@ -135,6 +151,61 @@ extern "C" int fr_debug_tc_raw(float* C, int K, int a_mn, int lbo, int sbo, fr_s
   const size_t smem = sizeof(float) * size_t(128 + 32) * K;
   cudaFuncSetAttribute(fr::tc_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   fr::tc_raw_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(C, K, a_mn, lbo, sbo);
+  ++fr::g_kernel_launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// Descriptor sweep: A smem (64 KB) holds ((word >> shift) & 1023) + 1, B = identity
+// (K-major), so C[m][k] names the word read for A(m, k) under raw descriptor
+// fields (layout type bits 61..63, a_mn selects MN-major).  Layout discovery only.
+namespace fr {
+__global__ void __launch_bounds__(128) tc_raw2_kernel(float* __restrict__ C, int a_mn, int lbo, int sbo, int ltype,
+                                                      int shift) {
+  extern __shared__ __align__(128) float sm2[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  constexpr int N = 32, K = 8, AW = 16384;
+  float* As = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sm2) + 1023) & ~uintptr_t(1023));
+  float* Bs = As + AW;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < AW; i += 128) As[i] = float(((i >> shift) & 1023) + 1);
+  for (int i = tid; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    Bs[(k >> 2) * (N * 4) + r * 4 + (k & 3)] = (r == k) ? 1.f : 0.f;
+  }
+  if (warp == 0) tc::tmem_alloc<32>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint64_t ad = tc::desc(As, lbo, sbo) | (uint64_t(ltype & 7) << 61);
+    tc::mma_tf32(tmem, ad, tc::desc(Bs, N * 16, 128), tc::idesc_tf32(128, N, a_mn, 0), 0);
+    tc::mma_commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+    for (int i = 0; i < 16; ++i) C[row * N + c0 + i] = v[i];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<32>(tmem);
+}
+}  // namespace fr
+
+extern "C" int fr_debug_tc_raw2(float* C, int a_mn, int lbo, int sbo, int ltype, int shift, fr_stream_t stream) {
+  const size_t smem = sizeof(float) * size_t(16384 + 32 * 8) + 1024;
+  cudaFuncSetAttribute(fr::tc_raw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  fr::tc_raw2_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(C, a_mn, lbo, sbo, ltype, shift);
   ++fr::g_kernel_launches;
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

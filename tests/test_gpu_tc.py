@@ -15,11 +15,15 @@ def _tf32(x):
     return (b & np.uint32(0xFFFFE000)).view(np.float32)
 
 
+@pytest.mark.parametrize("layout", [0, 5, 6, 7])
 @pytest.mark.parametrize("N,K", [(16, 8), (64, 32), (128, 64), (256, 64), (96, 40)])
-def test_tc_gemm_tf32(N, K):
-    """K-major A and B (the only TF32 operand layout the wide kernels use:
-    MN-major TF32 descriptors read zeros on sm_100a, tools/tc_layout_probe.py)."""
-    layout = 0
+def test_tc_gemm_tf32(N, K, layout):
+    """K-major A and B (layout 0, what the kernels use), and MN-major A / B / both
+    (5 / 6 / 7) in the SWIZZLE_128B_BASE32B canonical layout -- the only one in
+    which sm_100a reads MN-major TF32 (SWIZZLE_NONE MN-major reads zeros,
+    tools/tc_mn_probe.py); LBO = MN-group stride, SBO = K-group stride."""
+    if layout and N % 32:
+        pytest.skip("BASE32B MN-major atoms span 32 MN elements")
     import torch
 
     from paper_2602_15883_b200 import _lib as X

@@ -47,7 +47,8 @@ def main():
     for i, name in enumerate(PHASES):
         print(f"{i:2d} {name:28s} {buf[i] / tot * 100:6.2f}%")
     print("total CTA-cycles", tot)
-    for i, name in ((10, "tc3 dX A_lo transform"), (11, "tc3 MMA wait"), (12, "tc3 drain D")):
+    for i, name in ((10, "tc3 dX A_lo transform"), (11, "tc3 MMA wait"), (12, "tc3 drain D"), (13, "tc dW chunk wait"),
+                    (14, "tc dW staging"), (15, "tc dW stage barrier"), (9, "tc dW drain")):
         if buf[16 + i]:
             print(f"   {name:28s} {buf[16 + i] / tot * 100:6.2f}%")
 
