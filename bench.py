@@ -367,7 +367,7 @@ def run_ours(args):
         hbm = None
         if tf32:
             ntiles = -(-n_loc // (4 * (32 // (1 + rg.n_inputs + rg.n_space))))  # TcCfg::PPT
-            byts = tc_design_bytes(L, worker.plan.info.width_pad, ntiles)
+            byts = tc_design_bytes(L, worker.plan.info.tc_width, ntiles)
             peak_gbs = None
             try:
                 with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:

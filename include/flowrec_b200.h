@@ -59,6 +59,7 @@ typedef struct {
   int dtype, act, regime, num_sms;
   double inv_re;
   int math;          /* FR_MATH_* of the PDE / MSE training kernels */
+  int tc_width;      /* hidden width of the TF32 tcgen05 kernels (rounded to 16 / 32; 0: none) */
 } fr_plan_info;
 
 typedef struct {

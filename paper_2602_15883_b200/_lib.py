@@ -32,7 +32,7 @@ class PlanInfo(C.Structure):
         ("hidden_layers", C.c_int), ("width", C.c_int), ("width_pad", C.c_int),
         ("n_params", C.c_int), ("np_pad", C.c_int), ("kp_elems", C.c_int),
         ("dtype", C.c_int), ("act", C.c_int), ("regime", C.c_int), ("num_sms", C.c_int),
-        ("inv_re", C.c_double), ("math", C.c_int),
+        ("inv_re", C.c_double), ("math", C.c_int), ("tc_width", C.c_int),
     ]
 
 

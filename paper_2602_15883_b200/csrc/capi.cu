@@ -74,6 +74,7 @@ struct fr_plan {
   long long tcw_f = 0, tcw_d = 0;  // kp offsets of the tensor-core operand slabs (0: none)
   long long tc3 = 0;               // kp offset of the W=64 split-TF32 weight slabs (0: none)
   int tc_nb = 0;                   // N of the tensor-core MMAs (output units per CTA)
+  int tc_w = 0;                    // tensor width of the TF32 kernels (hidden width rounded to 16 / 32)
   int* d_inv = nullptr;      // kernel-param element -> real index or -1 [kp_elems]
 };
 
@@ -149,13 +150,21 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   // layer, per N block of NB units, per 16-deep K chunk, a contiguous K-major
   // [4 quads][NB][4] slab -- one for the forward (N = out units, K = in units)
   // and one for the adjoint (N = in units, K = out units)
+  // The TF32 kernels run on their own tensor width WT: the hidden width rounded
+  // up to the 16-deep K chunk (to 32 above 256 units, so that N = WT/2 is a
+  // multiple of 16), not to the 64-unit blocks of the SIMT layout -- padded
+  // units carry zero weights either way, so skipping them is exact (D150:
+  // 192 -> 160, E: 256 -> 208 units).  Parameters keep the 64-padded layout.
   const bool tc_ok = dtype == FR_F32 && wpad > 64 && wpad <= 512 && I.hidden_layers >= 2;
-  const int tc_nb = wpad <= 256 ? wpad : wpad / 2;
+  const int tc_w = width <= 256 ? (width + 15) / 16 * 16 : (width + 31) / 32 * 32;
+  const int tc_nb = tc_w <= 256 ? tc_w : tc_w / 2;
+  I.tc_width = tc_ok ? tc_w : 0;
   if (tc_ok) {
     p->tc_nb = tc_nb;
+    p->tc_w = tc_w;
     p->tcw_f = (I.kp_elems + 3) & ~3;
-    p->tcw_d = p->tcw_f + (long long)(I.hidden_layers - 1) * wpad * wpad;
-    I.kp_elems = int(p->tcw_d + (long long)(I.hidden_layers - 1) * wpad * wpad);
+    p->tcw_d = p->tcw_f + (long long)(I.hidden_layers - 1) * tc_w * tc_w;
+    I.kp_elems = int(p->tcw_d + (long long)(I.hidden_layers - 1) * tc_w * tc_w);
   }
   // W = 64 FP32 fused epoch kernel on the tensor cores (FR_MATH_TF32X3): per
   // hidden layer a forward [k/4][out][4] and an adjoint [k/4][in][4] K-major
@@ -178,7 +187,7 @@ extern "C" int fr_plan_create(const int* arch, int n_arch, int act, int regime, 
   // kernel (1.23x the FP32 SIMT epoch at config C, parity ~6e-7)
   I.math = tc_ok ? FR_MATH_TF32 : tc3_ok ? FR_MATH_TF32X3 : FR_MATH_SIMT;
   auto tc_slab = [&](long long base, int l, int n_unit, int k_unit) -> int {
-    const int nnb = wpad / tc_nb, nch = wpad / 16;
+    const int nnb = tc_w / tc_nb, nch = tc_w / 16;
     const int nb = n_unit / tc_nb, n = n_unit % tc_nb, c = k_unit / 16, kq = (k_unit % 16) / 4, j = k_unit % 4;
     return int(base + ((long long)((l - 1) * nnb + nb) * nch + c) * tc_nb * 16 + kq * tc_nb * 4 + n * 4 + j);
   };
@@ -360,7 +369,7 @@ struct WideSizes {
 static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WInfo* wi) {
   if (wide_call(p, mode, nullptr, nullptr, wi)) return 1;
   const fr_plan_info& I = p->info;
-  const long long L = I.hidden_layers, WP = I.width_pad;
+  const long long L = I.hidden_layers, WP = is_tc(p, mode) ? p->tc_w : I.width_pad;
   z->ntiles = (n + wi->ppt - 1) / wi->ppt;
   z->act = L * z->ntiles * WP * wi->rows;
   const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
@@ -451,7 +460,8 @@ static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* 
   a.n = n;
   a.ntiles = int(z.ntiles);
   a.L = I.hidden_layers;
-  a.WP = I.width_pad;
+  a.WP = is_tc(p, mode) ? p->tc_w : I.width_pad;
+  a.WK = I.width_pad;
   a.np_pad = I.np_pad;
   a.ks_rows = wide_ks(p, mode);
   if (is_tc(p, mode)) {

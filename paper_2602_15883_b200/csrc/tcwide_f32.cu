@@ -86,11 +86,15 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   const dim3 gw(a.WP / nbw, splits);
   for (int l = a.L - 1; l >= 1; --l)
     tcw_dw_kernel<ACT, MODE, REG><<<gw, C::DW_NT, stage * ns, st>>>(a, l, nbw, ns);
-  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
+  // per-tile partials are laid out on the tensor width WP; gpart on the
+  // parameter layout (width WK): dW_0 | db_0 rows of WP -> rows of WK, and
+  // dW_L (WP x NOUT) | db_L -> W_L rows then b_L at off_w(L) + WK * NOUT
+  const ParamLayout pl{C::DIN, a.WK, C::NOUT, a.L};
   const int len0 = (C::DIN + 1) * a.WP, lenL = a.WP * C::NOUT + C::NOUT;
-  tcw_partials_kernel<<<dim3((len0 + 255) / 256, ks), 256, 0, st>>>(a.p0, len0, a.ntiles, a.gpart, a.np_pad, pl.off_w(0));
+  tcw_partials_kernel<<<dim3((len0 + 255) / 256, ks), 256, 0, st>>>(a.p0, len0, a.ntiles, a.gpart, a.np_pad, pl.off_w(0),
+                                                                      a.WP, a.WK);
   tcw_partials_kernel<<<dim3((lenL + 255) / 256, ks), 256, 0, st>>>(a.pL, lenL, a.ntiles, a.gpart, a.np_pad,
-                                                                      pl.off_w(a.L));
+                                                                      pl.off_w(a.L), a.WP * C::NOUT, a.WK * C::NOUT);
   g_kernel_launches += 3 * (a.L - 1) + 3;
   return int(cudaGetLastError());
 }

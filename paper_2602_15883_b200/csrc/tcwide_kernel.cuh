@@ -116,11 +116,11 @@ __device__ __forceinline__ void tc_z0(const WArgs& a, const float* __restrict__ 
     const int u = 4 * q + j;
     float zv = 0.f;
 #pragma unroll
-    for (int i = 0; i < C::DIN; ++i) zv = fmaf(x[i], kp[pl.off_w(0) + i * a.WP + u], zv);
+    for (int i = 0; i < C::DIN; ++i) zv = fmaf(x[i], kp[pl.off_w(0) + i * a.WK + u], zv);
     z[0][j] = zv + kp[pl.off_b(0) + u];
     if constexpr (C::JET) {
 #pragma unroll
-      for (int i = 0; i < C::NG; ++i) z[1 + i][j] = kp[pl.off_w(0) + i * a.WP + u];
+      for (int i = 0; i < C::NG; ++i) z[1 + i][j] = kp[pl.off_w(0) + i * a.WK + u];
 #pragma unroll
       for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i][j] = 0.f;
     }
@@ -134,11 +134,11 @@ __device__ __forceinline__ void tc_z0u(const WArgs& a, const float* __restrict__
   const float* pts = static_cast<const float*>(a.pts);
   float zv = 0.f;
 #pragma unroll
-  for (int i = 0; i < C::DIN; ++i) zv = fmaf(p < a.n ? pts[p * C::DIN + i] : 0.f, kp[pl.off_w(0) + i * a.WP + u], zv);
+  for (int i = 0; i < C::DIN; ++i) zv = fmaf(p < a.n ? pts[p * C::DIN + i] : 0.f, kp[pl.off_w(0) + i * a.WK + u], zv);
   z[0] = zv + kp[pl.off_b(0) + u];
   if constexpr (C::JET) {
 #pragma unroll
-    for (int i = 0; i < C::NG; ++i) z[1 + i] = kp[pl.off_w(0) + i * a.WP + u];
+    for (int i = 0; i < C::NG; ++i) z[1 + i] = kp[pl.off_w(0) + i * a.WK + u];
 #pragma unroll
     for (int i = 0; i < C::NL; ++i) z[1 + C::NG + i] = 0.f;
   }
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
   const long long tile = blockIdx.x;
   const int nb = blockIdx.y, NB = a.nb, n0 = nb * NB;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
+  const ParamLayout pl{C::DIN, a.WK, C::NOUT, a.L};
   if (tid == 0)
     for (int i = 0; i < TC_NS; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
   const int NB = a.nb, nnb = a.WP / NB;
   const long long nitems = (long long)a.ntiles * nnb;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, C::NOUT, a.L};
+  const ParamLayout pl{C::DIN, a.WK, C::NOUT, a.L};
   if (tid == 0) {
     for (int i = 0; i < TCP_NS; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
   const long long tile = blockIdx.x;
   const int nb = blockIdx.y, NB = a.nb, n0 = nb * NB;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
+  const ParamLayout pl{DIN, a.WK, C::NOUT, a.L};
   if (tid == 0) {
     for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
     for (int i = 0; i < 2; ++i) {
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   const int NB = a.nb, nnb = a.WP / NB, nck = NB / 16;
   const long long nitems = (long long)a.ntiles * nnb;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{DIN, a.WP, C::NOUT, a.L};
+  const ParamLayout pl{DIN, a.WK, C::NOUT, a.L};
   if (tid == 0) {
     for (int i = 0; i < TCP_DX_NS; ++i) tc::mbar_init(&full[i], 1);
     for (int i = 0; i < 2; ++i) {
@@ -1036,7 +1036,7 @@ __global__ void __launch_bounds__(320) tcw_dw_kernel(WArgs a, int l, int NB, int
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nbk = blockIdx.x, n0 = nbk * NB, split = blockIdx.y;
   const int nkb = (WP + 127) / 128;
-  const ParamLayout pl{C::DIN, WP, C::NOUT, a.L};
+  const ParamLayout pl{C::DIN, a.WK, C::NOUT, a.L};
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(320) tcw_dw_kernel(WArgs a, int l, int NB, int
           float v[16];
           tc::tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + kb * NB + c0, v);
           if (kr < WP) {
-            double* dst = gp + pl.off_w(l) + size_t(kr) * WP + n0 + c0;
+            double* dst = gp + pl.off_w(l) + size_t(kr) * a.WK + n0 + c0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) dst[i] = double(v[i]);
           }
@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   const long long tile = blockIdx.x;
   const int tid = threadIdx.x;
   const float* kp = static_cast<const float*>(a.kp);
-  const ParamLayout pl{C::DIN, a.WP, NOUT, a.L};
+  const ParamLayout pl{C::DIN, a.WK, NOUT, a.L};
   const int L = a.L, nch = a.WP / TC_KC, ntot = 2 * nch;
   const float* zsrc = static_cast<const float*>(a.act) + tc_off(a, L - 1, tile, 0);
   if (tid == 0) {
@@ -1396,9 +1396,11 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
 }
 
 // fixed-order reduction of per-tile partials into the gradient-partial rows:
-// gpart[ks][off + i] = sum over tiles t = ks, ks + KS, ... of P[t][i]
+// gpart[ks][off + (i / w) * wk + i % w] = sum over tiles t = ks, ks + KS, ... of
+// P[t][i] (rows of w tensor-width entries land on rows of wk parameter-layout
+// entries)
 __global__ void __launch_bounds__(256) tcw_partials_kernel(const float* __restrict__ P, int len, long long ntiles,
-                                                           double* gpart, int np_pad, int off) {
+                                                           double* gpart, int np_pad, int off, int w, int wk) {
   const int i = blockIdx.x * 256 + threadIdx.x, ks = blockIdx.y, KS = gridDim.y;
   if (i >= len) return;
   double acc = 0.0;
@@ -1412,7 +1414,7 @@ __global__ void __launch_bounds__(256) tcw_partials_kernel(const float* __restri
     acc += double(v3);
   }
   for (; t < ntiles; t += KS) acc += double(P[size_t(t) * len + i]);
-  gpart[size_t(ks) * np_pad + off + i] = acc;
+  gpart[size_t(ks) * np_pad + off + (i / w) * wk + i % w] = acc;
 }
 
 }  // namespace fr

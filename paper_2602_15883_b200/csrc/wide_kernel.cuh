@@ -90,6 +90,7 @@ struct WArgs {
   double* lpart;      // [tiles][2]
   long long n;
   int ntiles, L, WP, np_pad, ks_rows;
+  int WK;             // parameter-layout width (== WP except on the TF32 path, whose WP is the tensor width)
   double coef, pcoef, inv_re;
   double velw[4];
   int has_p;
