@@ -18,6 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflowrec_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
+# kept object files (incremental rebuilds); git- and gpurun-ignored
+OBJ_DIR = os.path.join(os.path.dirname(HERE), "build", "obj")
 
 SOURCES = (["capi.cu", "nccl_transport.cu", "wide_f32.cu", "wide_f64.cu", "tc_probe.cu", "tcwide_f32.cu"]
            + [f"jetmlp_{m}_{d}.cu" for m in ("pde", "epoch", "mse", "value", "jet", "gj") for d in ("f32", "f64")])
@@ -47,9 +49,32 @@ def needs_build():
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def _compile(src, defines=(), out_dir=OUT_DIR):
+def _includes(path, seen=None):
+    """The file and every local header it includes, transitively."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("#include \""):
+                name = line.split('"')[1]
+                for d in (os.path.dirname(path), CSRC, INCLUDE):
+                    cand = os.path.join(d, name)
+                    if os.path.exists(cand):
+                        _includes(cand, seen)
+                        break
+    return seen
+
+
+def _compile(src, defines=(), out_dir=OUT_DIR, force=False):
     obj = os.path.join(out_dir, os.path.splitext(src)[0] + ".o")
     extra = os.environ.get("FR_NVCC_EXTRA", "").split()  # side-build experiments only
+    if not force and not defines and not extra and out_dir == OBJ_DIR and os.path.exists(obj):
+        t = os.path.getmtime(obj)
+        if all(os.path.getmtime(f) <= t for f in _includes(os.path.join(CSRC, src))):
+            return obj, ""  # object up to date with its source and headers
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c", os.path.join(CSRC, src),
            "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,11 +91,13 @@ def build(force=False, jobs=None, verbose=False, defines=(), lib=None):
     lib = lib or LIB
     if not force and lib == LIB and not needs_build():
         return LIB
-    out_dir = os.path.dirname(os.path.abspath(lib))
+    keep = lib == LIB and not defines
+    out_dir = OBJ_DIR if keep else os.path.dirname(os.path.abspath(lib))
     os.makedirs(out_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(os.path.abspath(lib)), exist_ok=True)
     jobs = jobs or min(len(SOURCES), os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
-        results = list(ex.map(lambda src: _compile(src, defines, out_dir), SOURCES))
+        results = list(ex.map(lambda src: _compile(src, defines, out_dir, force), SOURCES))
     for obj, log in results:
         if verbose and log.strip():
             print(log, file=sys.stderr)
@@ -81,8 +108,9 @@ def build(force=False, jobs=None, verbose=False, defines=(), lib=None):
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, lib)
-    for o, _ in results:
-        os.remove(o)
+    if not keep:
+        for o, _ in results:
+            os.remove(o)
     return lib
 
 
