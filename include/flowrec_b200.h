@@ -311,6 +311,9 @@ int fr_debug_tc_gemm_tf32(const float* A, const float* B, float* C, int N, int K
  * their own indices) that one 128x32xK MMA reads under descriptor (lbo, sbo) */
 int fr_debug_tc_raw(float* C, int K, int a_mn, int lbo, int sbo, fr_stream_t stream);
 int fr_debug_tc_raw2(float* C, int a_mn, int lbo, int sbo, int ltype, int shift, fr_stream_t stream);
+/* TMA view probe: one 32-row group of a k-quad slab buffer through the k-quad tensor
+ * map (csrc/tma.cuh), shared memory dumped to dst */
+int fr_debug_tma_kquad(const float* src, float* dst, int WP, int ntiles, int tile, int g, fr_stream_t stream);
 
 /* running count of kernels enqueued by this library (host-side counter) */
 long long fr_kernel_launches(void);

@@ -130,6 +130,7 @@ _SIGS = {
     "fr_debug_tc_gemm_tf32": [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P],
     "fr_debug_tc_raw": [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P],
     "fr_debug_tc_raw2": [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P],
+    "fr_debug_tma_kquad": [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P],
 }
 EXPORTS = tuple(_SIGS) + ("fr_last_error", "fr_version", "fr_kernel_launches")
 
@@ -168,7 +169,7 @@ LAUNCHERS = frozenset({
     "fr_reduce_grad", "fr_reduce_loss", "fr_adam_step", "fr_pack_ghost", "fr_ghost_put", "fr_counter_add",
     "fr_pcg64_uniform",
     "fr_jet_act_forward",
-    "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32",
+    "fr_jet_act_backward", "fr_bench_ffma", "fr_debug_tc_gemm_tf32", "fr_debug_tma_kquad",
 })
 launch_count = 0
 

@@ -4,6 +4,7 @@
 #include "flowrec_b200.h"
 #include "jetmlp.cuh"
 #include "tcgen05.cuh"
+#include "tma.cuh"
 
 namespace fr {
 
@@ -206,6 +207,41 @@ extern "C" int fr_debug_tc_raw2(float* C, int a_mn, int lbo, int sbo, int ltype,
   const size_t smem = sizeof(float) * size_t(16384 + 32 * 8) + 1024;
   cudaFuncSetAttribute(fr::tc_raw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   fr::tc_raw2_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(C, a_mn, lbo, sbo, ltype, shift);
+  ++fr::g_kernel_launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// TMA view probe (tests/test_gpu_tc.py): one 32-row group of a k-quad slab
+// buffer [tiles][WP/4][128][4] through kquad_map, shared memory dumped
+// linearly to dst.
+namespace fr {
+__global__ void __launch_bounds__(128) tma_probe_kernel(const __grid_constant__ CUtensorMap map, float* __restrict__ dst,
+                                                        int WP, int tile, int g) {
+  extern __shared__ __align__(128) unsigned char tp_smem[];
+  float* sm = reinterpret_cast<float*>(tp_smem + ((1024u - (tc::smem_u32(tp_smem) & 1023u)) & 1023u));
+  __shared__ __align__(8) uint64_t mbar;
+  const int floats = 32 * WP;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc::mbar_expect_tx(&mbar, uint32_t(floats) * 4);
+    tc::tma_load3(sm, &map, 128 * g, 0, tile, &mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  for (int i = threadIdx.x; i < floats; i += 128) dst[i] = sm[i];
+}
+}  // namespace fr
+
+extern "C" int fr_debug_tma_kquad(const float* src, float* dst, int WP, int ntiles, int tile, int g,
+                                  fr_stream_t stream) {
+  CUtensorMap m;
+  if (fr::kquad_map(&m, src, WP, ntiles, 32, WP / 4)) return -10;
+  const size_t smem = sizeof(float) * size_t(32 * WP) + 1024;
+  cudaFuncSetAttribute(fr::tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  fr::tma_probe_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(m, dst, WP, tile, g);
   ++fr::g_kernel_launches;
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

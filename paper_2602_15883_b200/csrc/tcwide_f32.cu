@@ -24,6 +24,16 @@ static bool tc_persistent_dx() {
   }();
   return v;
 }
+// FR_TC_DWQ=0 selects the weight gradient from row-quad-major Zbar^T copies
+// written by the adjoint / head kernels (A/B measurements); default:
+// tcw_dwq_kernel reads Zbar straight from the k-quad adjoint slabs
+static bool tc_dwq() {
+  static const bool v = [] {
+    const char* e = getenv("FR_TC_DWQ");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 static int tc_num_sms() {
   static int n = 0;
   if (!n) {
@@ -44,7 +54,10 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
     info->stq = 0;
   }
   if (!ap) return 0;
-  const WArgs& a = *ap;
+  const bool dwq = tc_dwq() && ap->WP <= 256;  // tcw_dwq_kernel covers WP <= 256
+  WArgs av = *ap;
+  if (dwq) av.zt = nullptr;  // no Zbar^T copies
+  const WArgs& a = av;
   const int NB = a.nb;
   static bool attrs = false;
   if (!attrs) {
@@ -56,6 +69,7 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
                          int(tcp_dx_smem<C>(256)));
     cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tcw_head_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::head_smem(512)));
+    cudaFuncSetAttribute(tcw_dwq_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attrs = true;
   }
   const dim3 gt(a.ntiles, a.WP / NB);
@@ -80,12 +94,27 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   const int nkb = (a.WP + 127) / 128;
   int nbw = std::min(256, 512 / nkb) / 16 * 16;
   while (a.WP % nbw) nbw -= 16;
-  const size_t stage = C::dw_stage_bytes(a.WP, nbw);
-  const int ns = int(std::min<size_t>(TC_DW_MAXNS, (200 * 1024) / stage));
   const int splits = std::max(1, std::min(ks, 148 / (a.WP / nbw)));
   const dim3 gw(a.WP / nbw, splits);
-  for (int l = a.L - 1; l >= 1; --l)
-    tcw_dw_kernel<ACT, MODE, REG><<<gw, C::DW_NT, stage * ns, st>>>(a, l, nbw, ns);
+  if (dwq) {
+    // converters hold <= 8 quads of each operand per warp; TMEM: nkb x NB (rounded to 32)
+    if (a.WP > 256 || nkb * ((nbw + 31) / 32 * 32) > 512)
+      return int(cudaErrorInvalidValue);
+    const size_t stage = dwq_stage_bytes(a.WP, nbw);
+    // as many stages as fit (+ 1 KB for the alignment of the ring)
+    int ns = int(std::min<size_t>(DWQ_MAXNS, (225 * 1024) / stage));
+    if (const char* e = getenv("FR_DWQ_NS")) ns = std::max(1, std::min(ns, atoi(e)));  // debugging
+    // tensor map over the k-quad adjoint slabs ([L * tiles][WP/4][128][4])
+    CUtensorMap tmB;
+    if (kquad_map(&tmB, a.adj, a.WP, (long long)a.L * a.ntiles, 32, nbw / 4)) return int(cudaErrorNotSupported);
+    for (int l = a.L - 1; l >= 1; --l)
+      tcw_dwq_kernel<ACT, MODE, REG><<<gw, 320, stage * ns + 1024, st>>>(a, l, nbw, ns, tmB);
+  } else {
+    const size_t stage = C::dw_stage_bytes(a.WP, nbw);
+    const int ns = int(std::min<size_t>(TC_DW_MAXNS, (200 * 1024) / stage));
+    for (int l = a.L - 1; l >= 1; --l)
+      tcw_dw_kernel<ACT, MODE, REG><<<gw, C::DW_NT, stage * ns, st>>>(a, l, nbw, ns);
+  }
   // per-tile partials are laid out on the tensor width WP; gpart on the
   // parameter layout (width WK): dW_0 | db_0 rows of WP -> rows of WK, and
   // dW_L (WP x NOUT) | db_L -> W_L rows then b_L at off_w(L) + WK * NOUT

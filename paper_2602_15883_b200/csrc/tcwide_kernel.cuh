@@ -28,6 +28,7 @@
 // stage through tcgen05.commit on the stage's "empty" barrier.
 #pragma once
 #include "tcgen05.cuh"
+#include "tma.cuh"
 #include "wide_kernel.cuh"
 
 namespace fr {
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
     for (int c = 0; c < nch; ++c) {
       const int s = c % TC_NS;
       tc::mbar_wait(&actd[s], (c / TC_NS) & 1);
-      if (nb == 0) slab_store_t<C>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
+      if (nb == 0 && a.st) slab_store_t<C>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
       arrive(&std_[s]);
     }
   } else {
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = int(g % TCP_NS);
         tc::mbar_wait(&actd[s], uint32_t(g / TCP_NS) & 1);
-        if (st0) slab_store_t<C, QS>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
+        if (st0 && a.st) slab_store_t<C, QS>(ring + s * SF, a.st + tc_toff(a, l - 1, tile), a.WP, 16 * c, t);
         arrive(&std_[s]);
       }
     }
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
       tc::mbar_wait(&rdy[b], (j >> 1) & 1);
       const float* sg = stg + b * 2048;
       slab_copy_out(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
-      slab_store_t<C>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+      if (a.zt) slab_store_t<C>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
       arrive(&done[b]);
     }
   }
@@ -1002,7 +1003,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         tc::mbar_wait(&rdy[b], uint32_t(jg >> 1) & 1);
         const float* sg = stg + b * QSL;
         slab_copy_out<QS>(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
-        slab_store_t<C, QS>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+        if (a.zt) slab_store_t<C, QS>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
         arrive(&done[b]);
       }
     }
@@ -1113,6 +1114,159 @@ __global__ void __launch_bounds__(320) tcw_dw_kernel(WArgs a, int l, int NB, int
         for (int c0 = half * 16; c0 < NB; c0 += 32) {
           float v[16];
           tc::tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + kb * NB + c0, v);
+          if (kr < WP) {
+            double* dst = gp + pl.off_w(l) + size_t(kr) * a.WK + n0 + c0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dst[i] = double(v[i]);
+          }
+        }
+      }
+    }
+  }
+  tc_teardown<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// dW_l = sum_rows S_{l-1}^T Zbar_l (+ db_l) with Zbar_l read straight from the
+// k-quad adjoint slabs (no row-quad-major Zbar^T copy: the adjoint and head
+// kernels write one slab fewer per layer).  S_{l-1}^T still comes
+// row-quad-major from the forward, which activates S in shared memory anyway
+// (re-activating Z here measured slower: the jet activation is as costly as
+// the copy it saves).  Zbar_l is the B operand with K = rows, i.e. MN-major,
+// which sm_100a reads for TF32 only in the SWIZZLE_128B_BASE32B layout
+// (512-byte atoms of 4 rows x 32 units, 32-byte chunks XOR-swizzled by the row;
+// LBO = 32-unit group stride, SBO = 4-row group stride; tests/test_gpu_tc.py
+// layouts 6 / 7).  Per 32-row group:
+//   warp 0      loader: the S^T group (one bulk copy, K-major [8 rq][WP][4])
+//               and the group's 32 rows of the Zbar_l N block's quads (one
+//               tensor-map copy, csrc/tma.cuh) as a k-quad stage;
+//   warps 2..9  converters: the Zbar pieces (lane = row: conflict-free 16-byte
+//               loads) into registers, then in place as BASE32B (pad rows
+//               zeroed); db_l from its value rows;
+//   warp 1      MMA issuer: ceil(WP/128) M = 128 blocks of in-units x NB
+//               out-units (rounded to whole 32-unit groups) in TMEM.
+// grid (WP/NB, splits), one CTA per SM.  Bit-identical to tcw_dw_kernel.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int dwq_b_floats(int NB) { return (NB + 31) / 32 * 1024; }
+constexpr int DWQ_MAXNS = 6;
+__host__ __device__ constexpr size_t dwq_stage_bytes(int WP, int NB) {
+  return sizeof(float) * size_t(dwq_b_floats(NB) + WP * 32);
+}
+// float offset of element (mn, row) in a BASE32B operand of 32 K rows
+__device__ __forceinline__ int dwq_b32(int mn, int r) {
+  return (((mn >> 5) * 8 + (r >> 2)) << 7) + ((r & 3) << 5) + (((((mn & 31) >> 3) ^ r) & 3) << 3) + (mn & 7);
+}
+template <int ACT, int MODE, int REG>
+__global__ void __launch_bounds__(320, 1) tcw_dwq_kernel(WArgs a, int l, int NB, int NS,
+                                                         const __grid_constant__ CUtensorMap tmB) {
+  using C = TcCfg<ACT, MODE, REG>;
+  constexpr int S = C::S, PPW = C::PPW, VR = C::VR;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  const int WP = a.WP, nqb = NB / 4;
+  // stage: [S^T group][BASE32B Zbar]; WP * 128 bytes keep the BASE32B part 1 KB
+  // aligned, and the second M block's reads past the S^T group (rows >= WP,
+  // never drained) stay inside the stage
+  const int AF = WP * 32, SF = AF + dwq_b_floats(NB);
+  // BASE32B atoms are swizzled on absolute address bits: 1 KB-aligned ring
+  float* ring = reinterpret_cast<float*>(tc_smem + ((1024u - (tc::smem_u32(tc_smem) & 1023u)) & 1023u));
+  __shared__ __align__(8) uint64_t full[DWQ_MAXNS], conv[DWQ_MAXNS], empty[DWQ_MAXNS], done;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nbk = blockIdx.x, n0 = nbk * NB, split = blockIdx.y;
+  const int nkb = (WP + 127) / 128;
+  // MMA N: the N block rounded up to whole 32-unit BASE32B groups (the extra
+  // columns see stale shared memory and are never drained)
+  const int NBM = (NB + 31) / 32 * 32;
+  const ParamLayout pl{C::DIN, a.WK, C::NOUT, a.L};
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&conv[i], 1);
+      tc::mbar_init(&empty[i], 1 + 8);  // MMA commit + the 8 converter / db warps
+    }
+    tc::mbar_init(&done, 1);
+  }
+  const uint32_t tmem = tc_setup<512>(&tslot, nullptr, 0);
+  const long long my_tiles = split < a.ntiles ? (a.ntiles - 1 - split) / gridDim.y + 1 : 0;
+  const long long nchunks = 4 * my_tiles;
+  double* gp = a.gpart + size_t(split) * a.np_pad;
+  if (warp == 0) {
+    if (lane == 0)
+      for (long long ci = 0; ci < nchunks; ++ci) {
+        const int s = int(ci % NS);
+        const long long t = split + (ci >> 2) * gridDim.y;
+        const int g = int(ci & 3);
+        if (ci >= NS) tc::mbar_wait(&empty[s], ((ci - NS) / NS) & 1);
+        float* A = ring + size_t(s) * SF;
+        float* B = A + AF;
+        tc::mbar_expect_tx(&full[s], uint32_t(WP + NB) * 128);
+        tc::bulk_g2s(A, a.st + tc_toff(a, l - 1, t) + size_t(g) * 8 * WP * 4, WP * 128, &full[s]);
+        tc::tma_load3(B, &tmB, 128 * g, n0 / 4, int(l * a.ntiles + t), &full[s]);
+      }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, NBM, 0, 1);
+      for (long long ci = 0; ci < nchunks; ++ci) {
+        const int s = int(ci % NS);
+        tc::mbar_wait(&conv[s], (ci / NS) & 1);
+        tc::fence_after();
+        const float* A = ring + size_t(s) * SF;
+        const float* B = A + AF;
+        for (int kb = 0; kb < nkb; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_tf32(tmem + kb * NBM, tc::desc(A + kb * 512 + kk * 8 * WP, WP * 16, 128),
+                         tc::desc(B + kk * 256, 4096, 512) | (uint64_t(1) << 61), idesc, (ci || kk) ? 1u : 0u);
+        tc::mma_commit(&empty[s]);
+      }
+      if (nchunks > 0) tc::mma_commit(&done);
+    }
+  } else {
+    const int ct = tid - 64;  // 0..255
+    // converter warp cw owns unit quads cw, cw + 8, ...; lane = row of the group
+    const int cw = warp - 2, r = lane;
+    const bool live = r < VR;
+    constexpr int MAXQ = 8;  // quads per warp (NB <= 256)
+    auto cbar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    float db = 0.f;
+    for (long long ci = 0; ci < nchunks; ++ci) {
+      const int s = int(ci % NS);
+      float* B = ring + size_t(s) * SF + AF;
+      tc::mbar_wait(&full[s], (ci / NS) & 1);
+      float4 vb[MAXQ];
+#pragma unroll
+      for (int k = 0; k < MAXQ; ++k) {
+        const int q = cw + 8 * k;
+        if (q < nqb)
+          vb[k] = live ? *reinterpret_cast<const float4*>(B + q * 128 + r * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cbar();
+#pragma unroll
+      for (int k = 0; k < MAXQ; ++k) {
+        const int q = cw + 8 * k;
+        if (q < nqb) *reinterpret_cast<float4*>(B + dwq_b32(4 * q, r)) = vb[k];
+      }
+      tc::fence_proxy_async();
+      cbar();
+      if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&conv[s])) : "memory");
+      // db_l: value rows of Zbar_l, one unit per thread, in row order
+      if (ct < NB)
+#pragma unroll
+        for (int pp = 0; pp < PPW; ++pp) db += B[dwq_b32(ct, pp * S)];
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&empty[s])) : "memory");
+    }
+    if (nchunks > 0) {
+      if (ct < NB) gp[pl.off_b(l) + n0 + ct] = double(db);
+      tc::mbar_wait(&done, 0);
+      tc::fence_after();
+      // warps 2..9: TMEM lane quadrant warp % 4, column half (warp - 2) / 4
+      const int quad = warp & 3, half = (warp - 2) >> 2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int kr = kb * 128 + quad * 32 + lane;
+        for (int c0 = half * 16; c0 < NB; c0 += 32) {
+          float v[16];
+          tc::tmem_ld16(tmem + (uint32_t(quad * 32) << 16) + kb * NBM + c0, v);
           if (kr < WP) {
             double* dst = gp + pl.off_w(l) + size_t(kr) * a.WK + n0 + c0;
 #pragma unroll
@@ -1382,7 +1536,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     }
     __syncthreads();
     slab_copy_out<QS>(slab, static_cast<float*>(a.adj) + tc_off(a, L - 1, tile, 4 * c), tid);
-    slab_store_t<C, QS>(slab, a.zt + tc_toff(a, L - 1, tile), a.WP, 16 * c, tid);
+    if (a.zt) slab_store_t<C, QS>(slab, a.zt + tc_toff(a, L - 1, tile), a.WP, 16 * c, tid);
     for (int e = tid; e < 16 * NOUT; e += NT) {
       const int kq = e / (4 * NOUT), j = (e / NOUT) % 4, o = e % NOUT;
       float acc = 0.f;

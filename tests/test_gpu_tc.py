@@ -89,3 +89,47 @@ def test_tc_persistent_kernels_bit_identical_to_tile_kernels():
         res[mode] = r.stdout.split()
     assert len(res["persistent"]) == 3
     assert res["persistent"] == res["tile"]
+
+
+def test_tc_dw_from_kquad_slabs_bit_identical_to_transposed_copies():
+    """The weight gradient with Zbar read straight from the k-quad adjoint
+    slabs (default, tcw_dwq_kernel: BASE32B MN-major B operand, tensor-map
+    TMA) equals the one from the row-quad-major Zbar^T copies (FR_TC_DWQ=0):
+    same rows per K-step, pad rows zero, so losses and gradients are
+    bit-identical -- ragged last tile, 3D (N block not a multiple of 32),
+    steady, MSE."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, FR_ROOT=root, FR_TC_DWQ=mode)
+        r = subprocess.run([sys.executable, "-c", _PERSIST_SCRIPT], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = r.stdout.split()
+    assert len(res["1"]) == 3
+    assert res["1"] == res["0"]
+
+
+
+@pytest.mark.parametrize("WP", [128, 160, 208])
+def test_tma_kquad_view(WP):
+    """The tensor-map TMA view of a k-quad slab buffer (csrc/tma.cuh, what the
+    weight-gradient kernel loads with: one cp.async.bulk.tensor per operand
+    and 32-row group) lands a group as the [quad][row][4] stage."""
+    import torch
+
+    from paper_2602_15883_b200 import _lib as X
+
+    nt, nq = 3, WP // 4
+    rng = np.random.default_rng(WP)
+    src = rng.standard_normal((nt, nq, 128, 4)).astype(np.float32)
+    dS = torch.from_numpy(src).cuda()
+    for tile, g in ((2, 1), (0, 3)):
+        d0 = torch.zeros(32 * WP, dtype=torch.float32, device="cuda")
+        X.call("fr_debug_tma_kquad", dS.data_ptr(), d0.data_ptr(), WP, nt, tile, g, None)
+        torch.cuda.synchronize()
+        assert np.array_equal(d0.cpu().numpy().reshape(nq, 32, 4), src[tile, :, 32 * g:32 * g + 32, :])
