@@ -27,6 +27,7 @@ int epoch_entry_f32(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, 
 int wide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int wide_entry_f64(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
 int tcwide_entry_f32(int, int, int, const WArgs*, int, cudaStream_t, WInfo*);
+bool tcwide_needs_zt(int WP);
 int epoch_entry_f64(int, int, int, const EpochArgs*, int, cudaStream_t, KInfo*, int, int);
 }  // namespace fr
 
@@ -375,7 +376,7 @@ static int wide_sizes(const fr_plan* p, int mode, long long n, WideSizes* z, WIn
   const bool bwd = (mode == FR_MODE_PDE || mode == FR_MODE_MSE || mode == FR_MODE_GJ);
   // SIMT: activation stash; tensor cores: row-quad-major S_l and Zbar_l copies
   z->stash = !bwd ? 0
-             : is_tc(p, mode) ? 2 * L * z->ntiles * WP * 128
+             : is_tc(p, mode) ? (tcwide_needs_zt(int(WP)) ? 2 : 1) * L * z->ntiles * WP * 128
                               : L * z->ntiles * (WP / 64) * (long long)wi->stq * wi->nt;
   // SIMT: Ybar rows; tensor cores: per-tile dW_0|db_0 and dW_L|db_L partials
   z->ybar = !bwd ? 0
@@ -471,7 +472,7 @@ static int launch_wide(const fr_plan* p, int mode, WArgs& a, long long n, void* 
     a.p0 = static_cast<float*>(a.ybar);
     a.pL = a.p0 + size_t(z.ntiles) * (I.n_in + 1) * a.WP;
     a.st = static_cast<float*>(a.stash);
-    a.zt = a.st + size_t(a.L) * z.ntiles * a.WP * 128;
+    a.zt = tcwide_needs_zt(a.WP) ? a.st + size_t(a.L) * z.ntiles * a.WP * 128 : nullptr;
   }
   a.inv_re = I.inv_re;
   if (bwd) FR_CUDA(cudaMemsetAsync(a.gpart, 0, sizeof(double) * size_t(a.ks_rows) * I.np_pad, st), "gpart zero");

@@ -128,6 +128,10 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   return int(cudaGetLastError());
 }
 
+// row-quad-major Zbar^T copies are only written (and allocated) for the
+// transposed-copy weight gradient
+bool tcwide_needs_zt(int WP) { return !(tc_dwq() && WP <= 256); }
+
 int tcwide_entry_f32(int mode, int act, int reg, const WArgs* a, int ks, cudaStream_t st, WInfo* info) {
   auto go = [&](auto act_c, auto reg_c) -> int {
     constexpr int ACT = decltype(act_c)::value, REG = decltype(reg_c)::value;
