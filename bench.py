@@ -192,11 +192,12 @@ def measure_tf32_peak(torch):
 
 def tc_design_bytes(L, WP, ntiles):
     """HBM bytes one TF32 wide PDE launch moves by design: 128-row x WP fp32
-    slabs per tile (Z, Zbar, and their row-quad-major copies S^T / Zbar^T)."""
+    slabs per tile (Z, Zbar, and the row-quad-major copy S^T the weight
+    gradient reads; Zbar is read by dW straight from its k-quad slab)."""
     slabs = ((L - 1) * 2 + (L - 2)          # fwd: write Z_l and S_{l-1}^T, read Z_{l-1} (l >= 2)
-             + (L - 1) + 3 * (L - 2)        # dx: read Zbar_l; read Z_{l-1}, write Zbar_{l-1}, Zbar^T (l >= 2)
-             + 2 * (L - 1)                  # dW: read S^T and Zbar^T
-             + 4)                           # head: Z_{L-1} twice, write Zbar_{L-1} and its copy
+             + (L - 1) + 2 * (L - 2)        # dx: read Zbar_l; read Z_{l-1}, write Zbar_{l-1} (l >= 2)
+             + 2 * (L - 1)                  # dW: read S^T and Zbar
+             + 3)                           # head: Z_{L-1} twice, write Zbar_{L-1}
     return slabs * ntiles * 128 * WP * 4
 
 
