@@ -1467,6 +1467,27 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     pL[size_t(a.WP) * NOUT + tid] = acc;
   }
   // ---- adjoint: S-bar = Ybar W_L^T, act-bwd, dW_L partial ----
+  // a thread's points are the same in every chunk: their Ybar rows are read
+  // once into registers (per item and chunk they were the adjoint's main
+  // shared-memory traffic: 3D, SN = 32 floats per item)
+  constexpr int KH = HU ? 1 : (C::ITEMS + NT - 1) / NT;
+  float ybr[KH][SN];
+  if constexpr (HU) {
+    const int pt = (tid >> 2) % PPT;
+#pragma unroll
+    for (int e = 0; e < SN; ++e) ybr[0][e] = Ybs[pt * SN + e];
+  } else {
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int i = tid + k * NT;
+      if (i < C::ITEMS) {
+        int pt, kq;
+        C::fwd_item(i, pt, kq);
+#pragma unroll
+        for (int e = 0; e < SN; ++e) ybr[k][e] = Ybs[pt * SN + e];
+      }
+    }
+  }
   for (int c = 0; c < nch; ++c) {
     const int g = nch + c, s = g % TC_NS;
     float* slab = ring + s * SF;
@@ -1474,9 +1495,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     if constexpr (HU) {
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
         const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
-        float yb[SN];  // registers: the red / slab stores below may alias Ybs
-#pragma unroll
-        for (int e = 0; e < SN; ++e) yb[e] = Ybs[pt * SN + e];
+        const float(&yb)[SN] = ybr[0];
         const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
         float zz[S], bb[S], sa[S];
         slab_load1<C, QS>(zz, slab, pt, kq, j);
@@ -1499,13 +1518,14 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
         slab_store1<C, QS>(slab, pt, kq, j, bb);  // Zbar_{L-1} in place of Z_{L-1}
       }
     } else
-    for (int i = tid; i < C::ITEMS; i += NT) {
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int i = tid + k * NT;
+      if (i >= C::ITEMS) break;
       int pt, kq;
       C::fwd_item(i, pt, kq);
       const int q = 4 * c + kq;
-      float yb[SN];  // registers: the red / slab stores below may alias Ybs
-#pragma unroll
-      for (int e = 0; e < SN; ++e) yb[e] = Ybs[pt * SN + e];
+      const float(&yb)[SN] = ybr[k];
       float z[S][4], sb[S][4];
       slab_load<C, QS>(z, slab, pt, kq);
 #pragma unroll
