@@ -34,6 +34,13 @@ static bool tc_dwq() {
   }();
   return v;
 }
+static int tc_dx_cq() {
+  static const int v = [] {
+    const char* e = getenv("FR_TC_DX_CQ");
+    return (e && std::string(e) == "4") ? 4 : 8;
+  }();
+  return v;
+}
 static int tc_num_sms() {
   static int n = 0;
   if (!n) {
@@ -65,8 +72,10 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
     cudaFuncSetAttribute(tcw_fwdp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(float) * TCP_NS * C::fwdp_stage_floats(256)));
     cudaFuncSetAttribute(tcw_dx_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::gemm_smem(256)));
-    cudaFuncSetAttribute(tcw_dxp_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(tcp_dx_smem<C>(256)));
+    cudaFuncSetAttribute(tcw_dxp_kernel<ACT, MODE, REG, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(tcp_dx_smem<C, 4>(256)));
+    cudaFuncSetAttribute(tcw_dxp_kernel<ACT, MODE, REG, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         226 * 1024);
     cudaFuncSetAttribute(tcw_dw_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tcw_head_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::head_smem(512)));
     cudaFuncSetAttribute(tcw_dwq_kernel<ACT, MODE, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
@@ -85,7 +94,16 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   if (tc_persistent_dx()) {
     const long long items = (long long)a.ntiles * (a.WP / NB);
     const int grid = int(std::min<long long>(items, tc_num_sms()));
-    for (int l = a.L - 1; l >= 1; --l) tcw_dxp_kernel<ACT, MODE, REG><<<grid, TCP_DX_NT, tcp_dx_smem<C>(NB), st>>>(a, l);
+    // 32-unit epilogue steps where the buffers fit and the N block has no
+    // 16-unit tail (D150 dx 1.36 -> 1.20 ms; the 3D 208-unit blocks measured
+    // 2 % slower with the tail step); FR_TC_DX_CQ=4 forces 16
+    if (tc_dx_cq() == 8 && NB % 32 == 0 && tcp_dx_smem<C, 8>(NB) <= 226 * 1024) {
+      for (int l = a.L - 1; l >= 1; --l)
+        tcw_dxp_kernel<ACT, MODE, REG, 8><<<grid, TCP_DX_NT, tcp_dx_smem<C, 8>(NB), st>>>(a, l);
+    } else {
+      for (int l = a.L - 1; l >= 1; --l)
+        tcw_dxp_kernel<ACT, MODE, REG, 4><<<grid, TCP_DX_NT, tcp_dx_smem<C, 4>(NB), st>>>(a, l);
+    }
   } else {
     for (int l = a.L - 1; l >= 1; --l) tcw_dx_kernel<ACT, MODE, REG><<<gt, TC_DX_NT, C::gemm_smem(NB), st>>>(a, l);
   }

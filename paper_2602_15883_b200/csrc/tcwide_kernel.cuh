@@ -772,19 +772,21 @@ __global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
 // ---------------------------------------------------------------------------
 constexpr int TCP_DX_NS = 4;
 constexpr int TCP_DX_NT = 576;
-template <class C>
+// CQ: unit quads per epilogue step (4: 16 TMEM columns, 8: 32 -- half the
+// barrier / wait round trips per item; the last step of an N block may be 4)
+template <class C, int CQ>
 __host__ __device__ constexpr int tcp_dx_epi() {  // floats of one epilogue group's buffers
   // stg[2] + zc[2] slabs with padded unit quads (C::FQS, see the forward), or
   // (l == 1) stg[0] + the dW_0 reduction buffer
-  return 4 * 4 * C::FQS > 4 * C::FQS + C::PPT * 16 * (C::DIN + 1) ? 4 * 4 * C::FQS
-                                                                  : 4 * C::FQS + C::PPT * 16 * (C::DIN + 1);
+  return 4 * CQ * C::FQS > CQ * C::FQS + C::PPT * 4 * CQ * (C::DIN + 1) ? 4 * CQ * C::FQS
+                                                                        : CQ * C::FQS + C::PPT * 4 * CQ * (C::DIN + 1);
 }
-template <class C>
+template <class C, int CQ>
 __host__ __device__ constexpr size_t tcp_dx_smem(int NB) {
   // epilogue: stg[2] + zc[2] slabs, or (l == 1) stg[0] + the dW_0 reduction buffer
-  return sizeof(float) * (TCP_DX_NS * C::stage_floats(NB) + 2 * tcp_dx_epi<C>());
+  return sizeof(float) * (TCP_DX_NS * C::stage_floats(NB) + 2 * tcp_dx_epi<C, CQ>());
 }
-template <int ACT, int MODE, int REG>
+template <int ACT, int MODE, int REG, int CQ>
 __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   using C = TcCfg<ACT, MODE, REG>;
   constexpr int DIN = C::DIN, D1 = DIN + 1;
@@ -793,7 +795,8 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   __shared__ __align__(8) uint64_t full[TCP_DX_NS], empty[TCP_DX_NS], accf[2], acce[2], zfull_[2][2], rdy_[2][2], done_[2][2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NB = a.nb, nnb = a.WP / NB, nck = NB / 16;
+  const int NB = a.nb, nnb = a.WP / NB, nqi = NB / 4, nck = (nqi + CQ - 1) / CQ;
+  auto stepq = [&](int j) { return nqi - CQ * j < CQ ? nqi - CQ * j : CQ; };  // quads of step j
   const long long nitems = (long long)a.ntiles * nnb;
   const float* kp = static_cast<const float*>(a.kp);
   const ParamLayout pl{DIN, a.WK, C::NOUT, a.L};
@@ -817,10 +820,10 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   const int grp = warp >= 10 ? 1 : 0, wl = warp - 10 * grp;
   // epilogue slabs: unit quads QS floats apart (conflict-free act-bwd items
   // with fwd_item() and a conflict-free row-quad gather for Zbar^T)
-  constexpr int QS = C::FQS, QSL = 4 * QS;
-  float* stg = ring + TCP_DX_NS * SF + grp * tcp_dx_epi<C>();  // [2][4 kq (QS)][128][4]  S-bar / Zbar columns
-  float* zc = stg + 2 * QSL;          // [2][4 kq (QS)][128][4]  Z_{l-1} slabs
-  float* red = stg + QSL;             // l == 1: [PPT][4 kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
+  constexpr int QS = C::FQS, QSL = CQ * QS;
+  float* stg = ring + TCP_DX_NS * SF + grp * tcp_dx_epi<C, CQ>();  // [2][CQ kq (QS)][128][4]  S-bar / Zbar columns
+  float* zc = stg + 2 * QSL;          // [2][CQ kq (QS)][128][4]  Z_{l-1} slabs
+  float* red = stg + QSL;             // l == 1: [PPT][CQ kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
   uint64_t* zfull = zfull_[grp];
   uint64_t* rdy = rdy_[grp];
   uint64_t* done = done_[grp];
@@ -870,9 +873,9 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   } else if (wl < 4) {
     const int r = (warp & 3) * 32 + lane, et = r;
     const float* pts = static_cast<const float*>(a.pts);
-    // Z_{l-1} slab of step j of item w (16 units)
+    // Z_{l-1} slab of step j of item w (CQ quads)
     auto zslab = [&](long long w, int j) {
-      return static_cast<const float*>(a.act) + tc_off(a, l - 1, w / nnb, int(w % nnb) * NB / 4) + size_t(j) * 2048;
+      return static_cast<const float*>(a.act) + tc_off(a, l - 1, w / nnb, int(w % nnb) * NB / 4) + size_t(j) * CQ * 512;
     };
     auto prefetch = [&](long long w, int j, int b) {  // step j of item w into zc[b] (j may run into the next item)
       if (j >= nck) {
@@ -880,8 +883,9 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         j -= nck;
       }
       if (w >= nitems) return;
-      tc::mbar_expect_tx(&zfull[b], 8192);
-      for (int q = 0; q < 4; ++q) tc::bulk_g2s(zc + b * QSL + q * QS, zslab(w, j) + q * 512, 2048, &zfull[b]);
+      const int nq = stepq(j);
+      tc::mbar_expect_tx(&zfull[b], 2048 * nq);
+      for (int q = 0; q < nq; ++q) tc::bulk_g2s(zc + b * QSL + q * QS, zslab(w, j) + q * 512, 2048, &zfull[b]);
     };
     const long long w0 = blockIdx.x + (long long)grp * gridDim.x;
     if (!virt && et == 0 && w0 < nitems)
@@ -896,12 +900,14 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         const int b = virt ? 0 : int(jg & 1);
         float* sg = stg + b * QSL;
         if (!virt && jg >= 2) tc::mbar_wait(&done[b], uint32_t((jg - 2) >> 1) & 1);
-        {
+        const int nqj = stepq(j), nhj = nqj / 4;  // quads / 16-unit blocks of this step
+        for (int h = 0; h < nhj; ++h) {
           float v[16];
-          tc::tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + ab * 256 + 16 * j, v);
+          tc::tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + ab * 256 + 4 * CQ * j + 16 * h, v);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(sg + q * QS + r * 4) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            *reinterpret_cast<float4*>(sg + (4 * h + q) * QS + r * 4) =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
         if (j == nck - 1) {
           tc::fence_before();
@@ -911,12 +917,14 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
         const float* zs = zc + b * QSL;
         if constexpr (TcUnit<C, true, ACT>::ON) {
-          for (int i = et; i < TcUnit<C, true, ACT>::N; i += 128) {
-            const int jj = i & 3;
+          constexpr int NU = TcUnit<C, true, ACT>::N;
+          for (int i = et; i < nhj * NU; i += 128) {
+            const int jj = i & 3, hh = i / NU;
             int pt, kq;
-            C::fwd_item(i >> 2, pt, kq);
+            C::fwd_item((i - hh * NU) >> 2, pt, kq);
+            kq += 4 * hh;
             float z[C::S], sb[C::S], sa[C::S];
-            if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 16 * j + 4 * kq + jj, z);
+            if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 4 * (CQ * j + kq) + jj, z);
             else slab_load1<C, QS>(z, zs, pt, kq, jj);
             slab_load1<C, QS>(sb, sg, pt, kq, jj);
             tc_act_bwd1<C, ACT>(z, sb, sa);
@@ -925,7 +933,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
             } else {
               const long long p = tile * C::PPT + pt;
               const bool live = p < a.n;
-              float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+              float* rd = red + ((pt * CQ + kq) * 4 + jj) * D1;
               const float zv = live ? sb[0] : 0.f;
 #pragma unroll
               for (int ii = 0; ii < DIN; ++ii) {
@@ -937,10 +945,12 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
             }
           }
         } else
-        for (int i = et; i < C::ITEMS; i += 128) {
+        for (int i = et; i < nhj * C::ITEMS; i += 128) {
+          const int hh = i / C::ITEMS;
           int pt, kq;
-          C::fwd_item(i, pt, kq);
-          const int q = n0 / 4 + 4 * j + kq;
+          C::fwd_item(i - hh * C::ITEMS, pt, kq);
+          kq += 4 * hh;
+          const int q = n0 / 4 + CQ * j + kq;
           float z[C::S][4], sb[C::S][4];
           if (virt) tc_z0<C>(a, kp, pl, tile * C::PPT + pt, q, z);
           else slab_load<C, QS>(z, zs, pt, kq);
@@ -964,7 +974,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
             for (int ii = 0; ii < DIN; ++ii) x[ii] = live ? pts[p * DIN + ii] : 0.f;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              float* rd = red + ((pt * 4 + kq) * 4 + jj) * D1;
+              float* rd = red + ((pt * CQ + kq) * 4 + jj) * D1;
               const float zv = live ? sb[0][jj] : 0.f;
 #pragma unroll
               for (int ii = 0; ii < DIN; ++ii) {
@@ -981,11 +991,11 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
           if (et == 0) prefetch(w, j + 2, b);
           arrive(&rdy[b]);
         } else {
-          for (int e = et; e < 16 * D1; e += 128) {
+          for (int e = et; e < 4 * nqj * D1; e += 128) {
             const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
             float acc = 0.f;
-            for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * 4 + kq) * 4 + jj) * D1 + ii];
-            const int u = n0 + 16 * j + 4 * kq + jj;
+            for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * CQ + kq) * 4 + jj) * D1 + ii];
+            const int u = n0 + 4 * (CQ * j + kq) + jj;
             a.p0[size_t(tile) * (D1 * a.WP) + size_t(ii) * a.WP + u] = acc;
           }
           sync_e();
@@ -1002,8 +1012,11 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         const int b = int(jg & 1);
         tc::mbar_wait(&rdy[b], uint32_t(jg >> 1) & 1);
         const float* sg = stg + b * QSL;
-        slab_copy_out<QS>(sg, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + 4 * j), t);
-        if (a.zt) slab_store_t<C, QS>(sg, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 16 * j, t);
+        for (int h = 0; h < stepq(j) / 4; ++h) {
+          slab_copy_out<QS>(sg + 4 * h * QS, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + CQ * j + 4 * h),
+                            t);
+          if (a.zt) slab_store_t<C, QS>(sg + 4 * h * QS, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 4 * (CQ * j + 4 * h), t);
+        }
         arrive(&done[b]);
       }
     }

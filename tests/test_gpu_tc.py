@@ -133,3 +133,23 @@ def test_tma_kquad_view(WP):
         X.call("fr_debug_tma_kquad", dS.data_ptr(), d0.data_ptr(), WP, nt, tile, g, None)
         torch.cuda.synchronize()
         assert np.array_equal(d0.cpu().numpy().reshape(nq, 32, 4), src[tile, :, 32 * g:32 * g + 32, :])
+
+
+def test_tc_adjoint_32_unit_steps_bit_identical_to_16():
+    """The persistent adjoint's 32-unit epilogue steps (default where the
+    buffers fit; the last step of an N block may be 16 units, e.g. the 3D
+    208-unit case) compute exactly what 16-unit steps do (FR_TC_DX_CQ=4)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("8", "4"):
+        env = dict(os.environ, FR_ROOT=root, FR_TC_DX_CQ=mode)
+        r = subprocess.run([sys.executable, "-c", _PERSIST_SCRIPT], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = r.stdout.split()
+    assert len(res["8"]) == 3
+    assert res["8"] == res["4"]
