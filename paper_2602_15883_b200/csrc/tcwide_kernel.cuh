@@ -764,10 +764,12 @@ __global__ void __launch_bounds__(TC_DX_NT) tcw_dx_kernel(WArgs a, int l) {
 // persistent adjoint, hidden layer l >= 1 (same math as tcw_dx_kernel).  One
 // CTA per SM walks the (tile, N block) items grid-strided; the MMAs of item
 // i+1 accumulate in the second TMEM buffer while the epilogue drains item i.
-//   warps 0..3  epilogue: S-bar TMEM -> shared, Z_{l-1} act-bwd in place (the
-//               Z_{l-1} slabs are prefetched two 16-unit steps ahead, across
-//               item boundaries), l == 1: dW_0 | db_0 tile partials
-//   warps 4..7  writers: Zbar_{l-1} slabs to HBM in both layouts
+//   warps 0..7  epilogue group 0 (items 0, 2, ...), warps 10..17 group 1:
+//               S-bar TMEM -> shared (warp w: lane quadrant w % 4, 16-column
+//               blocks of parity w / 4), Z_{l-1} act-bwd in place over all 8
+//               warps (the Z_{l-1} slabs are prefetched two steps ahead, across
+//               item boundaries), then the step's Zbar_{l-1} slab to HBM;
+//               l == 1: dW_0 | db_0 tile partials instead
 //   warp 8      bulk-copy loader (Zbar_l + W_l slabs)    warp 9  MMA issuer
 // ---------------------------------------------------------------------------
 constexpr int TCP_DX_NS = 4;
@@ -792,7 +794,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   constexpr int DIN = C::DIN, D1 = DIN + 1;
   extern __shared__ __align__(128) unsigned char tc_smem[];
   float* ring = reinterpret_cast<float*>(tc_smem);
-  __shared__ __align__(8) uint64_t full[TCP_DX_NS], empty[TCP_DX_NS], accf[2], acce[2], zfull_[2][2], rdy_[2][2], done_[2][2];
+  __shared__ __align__(8) uint64_t full[TCP_DX_NS], empty[TCP_DX_NS], accf[2], acce[2], zfull_[2][2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NB = a.nb, nnb = a.WP / NB, nqi = NB / 4, nck = (nqi + CQ - 1) / CQ;
@@ -804,12 +806,8 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
     for (int i = 0; i < TCP_DX_NS; ++i) tc::mbar_init(&full[i], 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&accf[i], 1);
-      tc::mbar_init(&acce[i], 4);
-      for (int j = 0; j < 2; ++j) {
-        tc::mbar_init(&zfull_[i][j], 1);
-        tc::mbar_init(&rdy_[i][j], 4);
-        tc::mbar_init(&done_[i][j], 4);
-      }
+      tc::mbar_init(&acce[i], 8);  // the 8 warps of epilogue group i
+      for (int j = 0; j < 2; ++j) tc::mbar_init(&zfull_[i][j], 1);
     }
   }
   const uint32_t tmem = tc_setup<512>(&tslot, empty, TCP_DX_NS);
@@ -825,13 +823,11 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
   float* zc = stg + 2 * QSL;          // [2][CQ kq (QS)][128][4]  Z_{l-1} slabs
   float* red = stg + QSL;             // l == 1: [PPT][CQ kq][4 j][D1] dW_0 contributions (in place of stg[1], zc)
   uint64_t* zfull = zfull_[grp];
-  uint64_t* rdy = rdy_[grp];
-  uint64_t* done = done_[grp];
   auto arrive = [&](uint64_t* bar) {
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
   };
-  auto sync_e = [grp] { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+  auto sync_e = [grp] { asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory"); };
   if (warp == 8) {
     if (lane == 0) {
       long long g = 0;
@@ -870,8 +866,11 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         tc::mma_commit(&accf[b]);
       }
     }
-  } else if (wl < 4) {
-    const int r = (warp & 3) * 32 + lane, et = r;
+  } else {
+    // epilogue group: 8 warps, 256 threads.  Warp wl reads TMEM lane quadrant
+    // wl % 4 (tile rows r) and the 16-column blocks h % 2 == wl / 4 of a step;
+    // every thread then takes act-bwd items and the step's copy-out
+    const int et = wl * 32 + lane, half = wl >> 2, r = (warp & 3) * 32 + lane;
     const float* pts = static_cast<const float*>(a.pts);
     // Z_{l-1} slab of step j of item w (CQ quads)
     auto zslab = [&](long long w, int j) {
@@ -899,9 +898,8 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
       for (int j = 0; j < nck; ++j, ++jg) {
         const int b = virt ? 0 : int(jg & 1);
         float* sg = stg + b * QSL;
-        if (!virt && jg >= 2) tc::mbar_wait(&done[b], uint32_t((jg - 2) >> 1) & 1);
         const int nqj = stepq(j), nhj = nqj / 4;  // quads / 16-unit blocks of this step
-        for (int h = 0; h < nhj; ++h) {
+        for (int h = half; h < nhj; h += 2) {
           float v[16];
           tc::tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + ab * 256 + 4 * CQ * j + 16 * h, v);
 #pragma unroll
@@ -918,7 +916,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         const float* zs = zc + b * QSL;
         if constexpr (TcUnit<C, true, ACT>::ON) {
           constexpr int NU = TcUnit<C, true, ACT>::N;
-          for (int i = et; i < nhj * NU; i += 128) {
+          for (int i = et; i < nhj * NU; i += 256) {
             const int jj = i & 3, hh = i / NU;
             int pt, kq;
             C::fwd_item((i - hh * NU) >> 2, pt, kq);
@@ -945,7 +943,7 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
             }
           }
         } else
-        for (int i = et; i < nhj * C::ITEMS; i += 128) {
+        for (int i = et; i < nhj * C::ITEMS; i += 256) {
           const int hh = i / C::ITEMS;
           int pt, kq;
           C::fwd_item(i - hh * C::ITEMS, pt, kq);
@@ -989,9 +987,16 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         sync_e();
         if (!virt) {
           if (et == 0) prefetch(w, j + 2, b);
-          arrive(&rdy[b]);
+          // Zbar_{l-1} of this step to HBM (k-quad): 16-byte rows, quads 2 KB apart
+          float* dst = static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + CQ * j);
+          for (int e = et; e < nqj * 128; e += 256)
+            reinterpret_cast<float4*>(dst + (e >> 7) * 512)[e & 127] =
+                reinterpret_cast<const float4*>(sg + (e >> 7) * QS)[e & 127];
+          if (a.zt && et < 128)
+            for (int h = 0; h < nhj; ++h)
+              slab_store_t<C, QS>(sg + 4 * h * QS, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 4 * (CQ * j + 4 * h), et);
         } else {
-          for (int e = et; e < 4 * nqj * D1; e += 128) {
+          for (int e = et; e < 4 * nqj * D1; e += 256) {
             const int kq = e / (4 * D1), jj = (e / D1) % 4, ii = e % D1;
             float acc = 0.f;
             for (int pt = 0; pt < C::PPT; ++pt) acc += red[((pt * CQ + kq) * 4 + jj) * D1 + ii];
@@ -1000,24 +1005,6 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
           }
           sync_e();
         }
-      }
-    }
-  } else if (!virt) {
-    const int t = (wl - 4) * 32 + lane;
-    long long jg = 0;
-    for (long long w = blockIdx.x + (long long)grp * gridDim.x; w < nitems; w += 2 * gridDim.x) {
-      const long long tile = w / nnb;
-      const int n0 = int(w % nnb) * NB;
-      for (int j = 0; j < nck; ++j, ++jg) {
-        const int b = int(jg & 1);
-        tc::mbar_wait(&rdy[b], uint32_t(jg >> 1) & 1);
-        const float* sg = stg + b * QSL;
-        for (int h = 0; h < stepq(j) / 4; ++h) {
-          slab_copy_out<QS>(sg + 4 * h * QS, static_cast<float*>(a.adj) + tc_off(a, l - 1, tile, n0 / 4 + CQ * j + 4 * h),
-                            t);
-          if (a.zt) slab_store_t<C, QS>(sg + 4 * h * QS, a.zt + tc_toff(a, l - 1, tile), a.WP, n0 + 4 * (CQ * j + 4 * h), t);
-        }
-        arrive(&done[b]);
       }
     }
   }
