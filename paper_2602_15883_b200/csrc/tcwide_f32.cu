@@ -94,10 +94,9 @@ int run_tcwide(const WArgs* ap, int ks, cudaStream_t st, WInfo* info) {
   if (tc_persistent_dx()) {
     const long long items = (long long)a.ntiles * (a.WP / NB);
     const int grid = int(std::min<long long>(items, tc_num_sms()));
-    // 32-unit epilogue steps where the buffers fit and the N block has no
-    // 16-unit tail (D150 dx 1.36 -> 1.20 ms; the 3D 208-unit blocks measured
-    // 2 % slower with the tail step); FR_TC_DX_CQ=4 forces 16
-    if (tc_dx_cq() == 8 && NB % 32 == 0 && tcp_dx_smem<C, 8>(NB) <= 226 * 1024) {
+    // 32-unit epilogue steps where the buffers fit (D150 dx 1.36 -> 1.20 ms;
+    // an N block of 208 ends with a 16-unit step); FR_TC_DX_CQ=4 forces 16
+    if (tc_dx_cq() == 8 && tcp_dx_smem<C, 8>(NB) <= 226 * 1024) {
       for (int l = a.L - 1; l >= 1; --l)
         tcw_dxp_kernel<ACT, MODE, REG, 8><<<grid, TCP_DX_NT, tcp_dx_smem<C, 8>(NB), st>>>(a, l);
     } else {

@@ -169,6 +169,50 @@ __device__ __forceinline__ void slab_store1(float* slab, int pt, int kq, int j, 
   for (int s = 0; s < C::S; ++s) b[4 * s] = v[s];
 }
 
+// v[s] <- v[s ^ x] (S a power of two, 0 <= x < S) with conditional swaps
+template <int S>
+__device__ __forceinline__ void xperm(float (&v)[S], int x) {
+#pragma unroll
+  for (int b = 1; b < S; b <<= 1) {
+    const bool f = (x & b) != 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (!(k & b)) {
+        const float t0 = v[k], t1 = v[k | b];
+        v[k] = f ? t1 : t0;
+        v[k | b] = f ? t0 : t1;
+      }
+  }
+}
+// slab_load1 / slab_store1 with the stream order XOR-permuted by x: lanes that
+// hold different points of one 8-stream (3D) tile touch different banks on
+// every instruction (a point's 8 rows are 128 bytes: the same banks otherwise)
+template <class C, int QS = 512>
+__device__ __forceinline__ void slab_load1x(float (&v)[C::S], const float* slab, int pt, int kq, int j, int x) {
+  if constexpr (C::S == 8) {
+    const float* b = slab + kq * QS + C::row0(pt) * 4 + j;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = b[4 * (s ^ x)];
+    xperm<8>(v, x);
+  } else {
+    slab_load1<C, QS>(v, slab, pt, kq, j);
+  }
+}
+template <class C, int QS = 512>
+__device__ __forceinline__ void slab_store1x(float* slab, int pt, int kq, int j, const float (&v)[C::S], int x) {
+  if constexpr (C::S == 8) {
+    float w[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) w[s] = v[s];
+    xperm<8>(w, x);
+    float* b = slab + kq * QS + C::row0(pt) * 4 + j;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) b[4 * (s ^ x)] = w[s];
+  } else {
+    slab_store1<C, QS>(slab, pt, kq, j, v);
+  }
+}
+
 // jet activation of one point / unit: s = sigma applied to the stacked jet
 template <class C, int ACT>
 __device__ __forceinline__ void tc_act1(const float (&z)[C::S], float (&s)[C::S]) {
@@ -557,8 +601,12 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
         float* A = ring + s * SF;
         tc::mbar_wait(&full[s], uint32_t(g / TCP_NS) & 1);
         if constexpr (TcUnit<C>::ON) {
+          // (unit, quad) fastest within a warp: 2 points per warp, 2-way bank
+          // conflicts with the FQS-padded quads (point-fastest lanes: 8-way;
+          // E fwd 2.84 -> 1.96 ms per launch; XOR-permuting the two points'
+          // stream orders as in the head measured 3 % slower)
           for (int i = t; i < TcUnit<C>::N; i += 128) {
-            const int j = i & 3, pt = (i >> 2) % C::PPT, kq = (i >> 2) / C::PPT;
+            const int j = i & 3, kq = (i >> 2) & 3, pt = i >> 4;
             float z[C::S], sv[C::S];
             if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, 16 * c + 4 * kq + j, z);
             else slab_load1<C, QS>(z, A, pt, kq, j);
@@ -915,12 +963,22 @@ __global__ void __launch_bounds__(TCP_DX_NT, 1) tcw_dxp_kernel(WArgs a, int l) {
         if (!virt) tc::mbar_wait(&zfull[b], uint32_t(jg >> 1) & 1);
         const float* zs = zc + b * QSL;
         if constexpr (TcUnit<C, true, ACT>::ON) {
+          // 3D: (unit, quad) fastest within a warp -- with the FQS-padded quads
+          // an 8-quad step's 32 lanes hit 32 distinct banks on every stream row
+          // (point-fastest lanes shared one bank group: a point's 8 rows are
+          // 128 bytes; E dx 3.78 -> 2.29 ms); 2D keeps the fwd_item lane map
           constexpr int NU = TcUnit<C, true, ACT>::N;
           for (int i = et; i < nhj * NU; i += 256) {
-            const int jj = i & 3, hh = i / NU;
+            const int jj = i & 3;
             int pt, kq;
-            C::fwd_item((i - hh * NU) >> 2, pt, kq);
-            kq += 4 * hh;
+            if constexpr (C::FWD_MAP) {
+              const int hh = i / NU;
+              C::fwd_item((i - hh * NU) >> 2, pt, kq);
+              kq += 4 * hh;
+            } else {
+              kq = (i >> 2) % nqj;
+              pt = (i >> 2) / nqj;
+            }
             float z[C::S], sb[C::S], sa[C::S];
             if (virt) tc_z0u<C>(a, kp, pl, tile * C::PPT + pt, n0 + 4 * (CQ * j + kq) + jj, z);
             else slab_load1<C, QS>(z, zs, pt, kq, jj);
@@ -1339,7 +1397,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
         const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
         float zz[S], ss[S];
-        slab_load1<C, QS>(zz, ring + s * SF, pt, kq, j);
+        slab_load1x<C, QS>(zz, ring + s * SF, pt, kq, j, pt & 7);
         tc_act1<C, ACT>(zz, ss);
         const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
 #pragma unroll
@@ -1498,7 +1556,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
         const float(&yb)[SN] = ybr[0];
         const float* w = WLs + (16 * c + 4 * kq + j) * NOUT;
         float zz[S], bb[S], sa[S];
-        slab_load1<C, QS>(zz, slab, pt, kq, j);
+        slab_load1x<C, QS>(zz, slab, pt, kq, j, pt & 7);
 #pragma unroll
         for (int st = 0; st < S; ++st) {
           float v = 0.f;
@@ -1515,7 +1573,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
           for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
           rd[o] = v;
         }
-        slab_store1<C, QS>(slab, pt, kq, j, bb);  // Zbar_{L-1} in place of Z_{L-1}
+        slab_store1x<C, QS>(slab, pt, kq, j, bb, pt & 7);  // Zbar_{L-1} in place of Z_{L-1}
       }
     } else
 #pragma unroll
