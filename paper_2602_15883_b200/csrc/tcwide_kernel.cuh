@@ -33,7 +33,11 @@
 
 namespace fr {
 
-constexpr int TC_NS = 4;   // fwd / dx / head ring stages
+constexpr int TC_NS = 4;   // fwd / dx ring stages
+#ifndef FR_TC_HEAD_NS
+#define FR_TC_HEAD_NS 2  // 2 stages -> more CTAs per SM: E head 3.37 -> 3.04, D150 1.12 -> 1.01 ms (4: the old ring)
+#endif
+constexpr int TC_HEAD_NS = FR_TC_HEAD_NS;  // head ring stages
 constexpr int TC_KC = 16;  // K depth of one stage (4 unit quads)
 
 template <int ACT, int MODE, int REG>
@@ -96,7 +100,7 @@ struct TcCfg {
   static constexpr int HEAD_RED = 4 * NOUT * HRS;
   __host__ __device__ static size_t head_smem(int WP) {
     return sizeof(double) * 2 * NT +
-           sizeof(float) * size_t(TC_NS * 4 * FQS + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
+           sizeof(float) * size_t(TC_HEAD_NS * 4 * FQS + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
   }
 };
 
@@ -1355,12 +1359,12 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   double* lred = reinterpret_cast<double*>(tc_smem);      // [2][NT]
   constexpr int QS = C::FQS, SF = 4 * QS;                 // padded unit quads (see TcCfg::FQS)
   float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][4][QS]
-  float* WLs = ring + TC_NS * SF;                          // [WP][NOUT]
+  float* WLs = ring + TC_HEAD_NS * SF;                          // [WP][NOUT]
   float* Yp = WLs + a.WP * NOUT;                           // [NT][SN]
   float* Ys = Yp + NT * SN;                                // [PPT][SN]
   float* Ybs = Ys + PPT * SN;                              // [PPT][SN]
   float* red = Ybs + PPT * SN;                             // see TcCfg::HEAD_RED
-  __shared__ __align__(8) uint64_t full[TC_NS];
+  __shared__ __align__(8) uint64_t full[TC_HEAD_NS];
   const long long tile = blockIdx.x;
   const int tid = threadIdx.x;
   const float* kp = static_cast<const float*>(a.kp);
@@ -1368,19 +1372,19 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   const int L = a.L, nch = a.WP / TC_KC, ntot = 2 * nch;
   const float* zsrc = static_cast<const float*>(a.act) + tc_off(a, L - 1, tile, 0);
   if (tid == 0) {
-    for (int i = 0; i < TC_NS; ++i) tc::mbar_init(&full[i], 1);
+    for (int i = 0; i < TC_HEAD_NS; ++i) tc::mbar_init(&full[i], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
   auto produce = [&](int g) {
-    const int s = g % TC_NS;
+    const int s = g % TC_HEAD_NS;
     tc::mbar_expect_tx(&full[s], 8192);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       tc::bulk_g2s(ring + s * SF + q * QS, zsrc + size_t(g % nch) * 2048 + q * 512, 2048, &full[s]);
   };
   if (tid == 0)
-    for (int g = 0; g < TC_NS && g < ntot; ++g) produce(g);
+    for (int g = 0; g < TC_HEAD_NS && g < ntot; ++g) produce(g);
   for (int i = tid; i < a.WP * NOUT; i += NT) WLs[i] = kp[pl.off_w(L) + i];
   __syncthreads();
   // ---- forward: Y partials per (point, kq) thread ----
@@ -1390,8 +1394,8 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) y[st][o] = 0.f;
   for (int c = 0; c < nch; ++c) {
-    const int s = c % TC_NS;
-    tc::mbar_wait(&full[s], (c / TC_NS) & 1);
+    const int s = c % TC_HEAD_NS;
+    tc::mbar_wait(&full[s], (c / TC_HEAD_NS) & 1);
     if constexpr (HU) {
       // per-unit items: thread tid always holds point (tid >> 2) % PPT
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
@@ -1424,7 +1428,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       }
     }
     __syncthreads();
-    if (tid == 0 && c + TC_NS < ntot) produce(c + TC_NS);
+    if (tid == 0 && c + TC_HEAD_NS < ntot) produce(c + TC_HEAD_NS);
   }
 #pragma unroll
   for (int st = 0; st < S; ++st)
@@ -1547,9 +1551,9 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     }
   }
   for (int c = 0; c < nch; ++c) {
-    const int g = nch + c, s = g % TC_NS;
+    const int g = nch + c, s = g % TC_HEAD_NS;
     float* slab = ring + s * SF;
-    tc::mbar_wait(&full[s], (g / TC_NS) & 1);
+    tc::mbar_wait(&full[s], (g / TC_HEAD_NS) & 1);
     if constexpr (HU) {
       for (int i = tid; i < 4 * C::ITEMS; i += NT) {
         const int j = i & 3, pt = (i >> 2) % PPT, kq = (i >> 2) / PPT;
@@ -1623,7 +1627,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       pL[size_t(16 * c + 4 * kq + j) * NOUT + o] = acc;
     }
     __syncthreads();
-    if (tid == 0 && g + TC_NS < ntot) produce(g + TC_NS);
+    if (tid == 0 && g + TC_HEAD_NS < ntot) produce(g + TC_HEAD_NS);
   }
 }
 
