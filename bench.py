@@ -367,7 +367,7 @@ def run_ours(args):
         achieved = flops_launch / pde["ms"] * 1e-9  # TFLOP/s
         hbm = None
         if tf32:
-            ntiles = -(-n_loc // (4 * (32 // (1 + rg.n_inputs + rg.n_space))))  # TcCfg::PPT
+            ntiles = -(-n_loc // (128 // (1 + rg.n_inputs + rg.n_space)))  # TcCfg::PPT
             byts = tc_design_bytes(L, worker.plan.info.tc_width, ntiles)
             peak_gbs = None
             try:

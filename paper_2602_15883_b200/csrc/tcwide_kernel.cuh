@@ -6,10 +6,10 @@
 // accumulator in TMEM.  All operands are K-major SWIZZLE_NONE UMMA tiles
 // (TF32 MN-major descriptors read zeros on sm_100a, see tools/tc_layout_probe.py).
 //
-// Tile geometry.  A tile is one 128-row MMA block: four 32-row groups, each
-// holding PPW = 32/S points x S jet streams (rows p*S+s) plus 32 - PPW*S pad
-// rows.  Pad rows are never read by the per-point code; the dW kernel zeroes
-// them before they reach the tensor core.
+// Tile geometry.  A tile is one 128-row MMA block packing PPT = 128 / S
+// points x S jet streams (rows p*S+s) plus 128 - PPT*S pad rows (2D PDE: 21
+// points and 2 pad rows).  Pad rows are never read by the per-point code; the
+// weight-gradient operands zero them before they reach the tensor core.
 //
 // HBM buffers (fp32, k-quad layout [layer][tile][WP/4][128][4], one quad of a
 // tile = 2 KB contiguous = a K-major 128 x 4 operand slab):
@@ -49,12 +49,15 @@ struct TcCfg {
   static constexpr bool JET = St::JET;
   static constexpr int NT = 128;              // fwd / dx / head CTAs (one thread per TMEM lane)
   static constexpr int DW_NT = 320;           // dW CTAs (loader, MMA, 8 drain / db warps)
-  static constexpr int PPW = 32 / S;          // points per 32-row group
-  static constexpr int PPT = 4 * PPW;         // points per tile
-  static constexpr int VR = PPW * S;          // valid rows per 32-row group
+  // a tile packs PPT = 128 / S points' jet rows (row p * S + s); rows >= VRT
+  // are pad rows (2D PDE: 21 points, rows 126 / 127; 3D: 16 points, none)
+  static constexpr int PPT = 128 / S;         // points per tile
+  static constexpr int VRT = PPT * S;         // valid rows of a tile
   static constexpr int ITEMS = PPT * 4;       // (point, unit quad) items of one 16-deep chunk
   static constexpr int TPP = ITEMS <= NT ? 4 : 1;  // threads holding partial sums of one point (head)
-  __host__ __device__ static constexpr int row0(int pt) { return (pt / PPW) * 32 + (pt % PPW) * S; }
+  __host__ __device__ static constexpr int row0(int pt) { return pt * S; }
+  // a value row (the point's z_v: gets the bias, feeds db)
+  __host__ __device__ static constexpr bool vrow(int r) { return r < VRT && r % S == 0; }
   __host__ __device__ static constexpr size_t stage_floats(int NB) { return 2048 + size_t(NB) * 16; }
   // persistent forward: the activation slab's unit quads are FQS floats apart
   // (128 rows x 4 + 4): quad q shifts every row by 4 banks, which makes the St
@@ -62,21 +65,20 @@ struct TcCfg {
   // 16-byte loads / stores nearly so (tools/bank_model.py)
   static constexpr int FQS = 516;
   __host__ __device__ static constexpr size_t fwdp_stage_floats(int NB) { return 4 * FQS + size_t(NB) * 16; }
-  // (point, unit quad) of activation item i: each 8-lane phase takes 4 points of
-  // one 32-row group x 2 quads, whose 16-byte rows then fall in 8 distinct
-  // bank groups (rows 6p mod 8 = {0,6,4,2}, quads +1); the 4th point of every
-  // group (rows 24..29, residue 0) fills the last two phases
-  static constexpr bool FWD_MAP = (PPW == 5 && PPT == 20 && ITEMS == 80);
+  // (point, unit quad) of activation item i (2D PDE, S = 6): each 8-lane phase
+  // takes 4 consecutive points x 2 quads, whose 16-byte rows then fall in 8
+  // distinct bank groups (rows 6p mod 8 = {0,6,4,2} + 6 * 4k, quads +1 with the
+  // FQS padding); the 21st point's 4 quads fill the last phase
+  static constexpr bool FWD_MAP = (S == 6 && PPT == 21 && ITEMS == 84);
   __device__ static void fwd_item(int i, int& pt, int& kq) {
     if constexpr (FWD_MAP) {
-      if (i < 64) {
+      if (i < 80) {
         const int ph = i >> 3, p8 = i & 7;
-        pt = 5 * (ph >> 1) + (p8 >> 1);
+        pt = 4 * (ph >> 1) + (p8 >> 1);
         kq = 2 * (ph & 1) + (p8 & 1);
       } else {
-        const int j = i - 64, p8 = j & 7;
-        pt = 5 * (2 * (j >> 3) + (p8 >> 2)) + 4;
-        kq = p8 & 3;
+        pt = 20;
+        kq = i - 80;
       }
     } else {
       pt = i % PPT;
@@ -86,8 +88,7 @@ struct TcCfg {
   // inverse of fwd_item: the item index that holds (pt, kq)
   __device__ static int item_of(int pt, int kq) {
     if constexpr (FWD_MAP) {
-      const int g = pt / 5, p = pt % 5;
-      return p < 4 ? 8 * (2 * g + (kq >> 1)) + 2 * p + (kq & 1) : 64 + 8 * (g >> 1) + 4 * (g & 1) + kq;
+      return pt < 20 ? 8 * (2 * (pt >> 2) + (kq >> 1)) + 2 * (pt & 3) + (kq & 1) : 80 + kq;
     } else {
       return kq * PPT + pt;
     }
@@ -317,7 +318,7 @@ __device__ __forceinline__ void slab_store_t(const float* slab, float* dstT, int
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
       const float x = src[rr * 4];
-      v[rr] = ((4 * rq + rr) & 31) < C::VR ? x : 0.f;
+      v[rr] = (4 * rq + rr) < C::VRT ? x : 0.f;
     }
     *reinterpret_cast<float4*>(dstT + (size_t(rq) * WP + k0 + k16) * 4) = make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(TC_FWD_NT) tcw_fwd_kernel(WArgs a, int l) {
     tc::mbar_wait(&mmad[(nch - 1) % TC_NS], ((nch - 1) / TC_NS) & 1);
     tc::fence_after();
     const int r = warp * 32 + lane;
-    const bool vrow = lane < C::VR && (lane % C::S) == 0;
+    const bool vrow = C::vrow(r);
     float* Zo = static_cast<float*>(a.act) + tc_off(a, l, tile, n0 / 4) + r * 4;
     const float* bl = kp + pl.off_b(l) + n0;
     for (int c0 = 0; c0 < NB; c0 += 16) {
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(TCP_FWD_NT, 1) tcw_fwdp_kernel(WArgs a, int l)
     }
   } else if (warp >= 14) {
     const int q = warp & 3, r = q * 32 + lane;
-    const bool vrow = lane < C::VR && (lane % C::S) == 0;
+    const bool vrow = C::vrow(r);
     long long it = 0;
     for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
       const long long tile = w / nnb;
@@ -1152,14 +1153,22 @@ __global__ void __launch_bounds__(320) tcw_dw_kernel(WArgs a, int l, int NB, int
     const int u = tid - 64;  // 0..255
     float db = 0.f;
     for (long long ci = 0; ci < nchunks; ++ci) {
-      const int s = int(ci % NS);
+      const int s = int(ci % NS), g = int(ci & 3);
       tc::mbar_wait(&full[s], (ci / NS) & 1);
       if (u < NB) {
         const float* B = ring + s * SF + WP * 32;
+        // value rows of the group, in row order: compile-time row lists per group
+        auto dbg = [&](auto G) {
+          constexpr int gg = decltype(G)::value, r0 = (S - (32 * gg) % S) % S;
 #pragma unroll
-        for (int pp = 0; pp < C::PPW; ++pp) {
-          const int r = pp * S;
-          db += B[((r >> 2) * NB + u) * 4 + (r & 3)];
+          for (int r = r0; r < 32; r += S)
+            if (C::vrow(32 * gg + r)) db += B[((r >> 2) * NB + u) * 4 + (r & 3)];
+        };
+        switch (g) {
+          case 0: dbg(IntC<0>{}); break;
+          case 1: dbg(IntC<1>{}); break;
+          case 2: dbg(IntC<2>{}); break;
+          default: dbg(IntC<3>{}); break;
         }
       }
       __syncwarp();
@@ -1222,7 +1231,7 @@ template <int ACT, int MODE, int REG>
 __global__ void __launch_bounds__(320, 1) tcw_dwq_kernel(WArgs a, int l, int NB, int NS,
                                                          const __grid_constant__ CUtensorMap tmB) {
   using C = TcCfg<ACT, MODE, REG>;
-  constexpr int S = C::S, PPW = C::PPW, VR = C::VR;
+  constexpr int S = C::S;
   extern __shared__ __align__(128) unsigned char tc_smem[];
   const int WP = a.WP, nqb = NB / 4;
   // stage: [S^T group][BASE32B Zbar]; WP * 128 bytes keep the BASE32B part 1 KB
@@ -1287,13 +1296,14 @@ __global__ void __launch_bounds__(320, 1) tcw_dwq_kernel(WArgs a, int l, int NB,
     const int ct = tid - 64;  // 0..255
     // converter warp cw owns unit quads cw, cw + 8, ...; lane = row of the group
     const int cw = warp - 2, r = lane;
-    const bool live = r < VR;
     constexpr int MAXQ = 8;  // quads per warp (NB <= 256)
     auto cbar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
     float db = 0.f;
     for (long long ci = 0; ci < nchunks; ++ci) {
       const int s = int(ci % NS);
       float* B = ring + size_t(s) * SF + AF;
+      const int g = int(ci & 3);
+      const bool live = 32 * g + r < C::VRT;  // pad rows carry zeros
       tc::mbar_wait(&full[s], (ci / NS) & 1);
       float4 vb[MAXQ];
 #pragma unroll
@@ -1312,9 +1322,21 @@ __global__ void __launch_bounds__(320, 1) tcw_dwq_kernel(WArgs a, int l, int NB,
       cbar();
       if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&conv[s])) : "memory");
       // db_l: value rows of Zbar_l, one unit per thread, in row order
-      if (ct < NB)
+      if (ct < NB) {
+        // value rows of group g, in row order: compile-time row lists per group
+        auto dbg = [&](auto G) {
+          constexpr int gg = decltype(G)::value, r0 = (S - (32 * gg) % S) % S;
 #pragma unroll
-        for (int pp = 0; pp < PPW; ++pp) db += B[dwq_b32(ct, pp * S)];
+          for (int rr = r0; rr < 32; rr += S)
+            if (C::vrow(32 * gg + rr)) db += B[dwq_b32(ct, rr)];
+        };
+        switch (g) {
+          case 0: dbg(IntC<0>{}); break;
+          case 1: dbg(IntC<1>{}); break;
+          case 2: dbg(IntC<2>{}); break;
+          default: dbg(IntC<3>{}); break;
+        }
+      }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&empty[s])) : "memory");
     }
