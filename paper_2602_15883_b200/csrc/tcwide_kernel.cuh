@@ -98,10 +98,16 @@ struct TcCfg {
   // head dW_L partials: [pt][kq][j][o] for per-unit items, else [j][o][item]
   // rows of HRS = ITEMS + 1 floats (lane-contiguous stores, odd row stride)
   static constexpr int HRS = ITEMS + 1;
-  static constexpr int HEAD_RED = 4 * NOUT * HRS;
+  // per-unit items (3D): [16 units][NOUT][point], point rows RSP apart so the 8
+  // points x 4 units of a warp's stores hit 32 distinct banks
+  static constexpr int RSP = PPT + 2;
+  static constexpr int HEAD_RED = 4 * NOUT * HRS > 16 * NOUT * RSP ? 4 * NOUT * HRS : 16 * NOUT * RSP;
+  // Y partial rows: SN + 1 floats apart (a stride of SN = 32 put every lane's
+  // stores in one bank)
+  static constexpr int YPS = S * NOUT + 1;
   __host__ __device__ static size_t head_smem(int WP) {
     return sizeof(double) * 2 * NT +
-           sizeof(float) * size_t(TC_HEAD_NS * 4 * FQS + WP * NOUT + NT * S * NOUT + 2 * PPT * S * NOUT + HEAD_RED);
+           sizeof(float) * size_t(TC_HEAD_NS * 4 * FQS + WP * NOUT + NT * YPS + 2 * PPT * S * NOUT + HEAD_RED);
   }
 };
 
@@ -1382,8 +1388,8 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
   constexpr int QS = C::FQS, SF = 4 * QS;                 // padded unit quads (see TcCfg::FQS)
   float* ring = reinterpret_cast<float*>(lred + 2 * NT);  // [NS][4][QS]
   float* WLs = ring + TC_HEAD_NS * SF;                          // [WP][NOUT]
-  float* Yp = WLs + a.WP * NOUT;                           // [NT][SN]
-  float* Ys = Yp + NT * SN;                                // [PPT][SN]
+  float* Yp = WLs + a.WP * NOUT;                           // [NT][YPS]
+  float* Ys = Yp + NT * C::YPS;                            // [PPT][SN]
   float* Ybs = Ys + PPT * SN;                              // [PPT][SN]
   float* red = Ybs + PPT * SN;                             // see TcCfg::HEAD_RED
   __shared__ __align__(8) uint64_t full[TC_HEAD_NS];
@@ -1455,7 +1461,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
 #pragma unroll
   for (int st = 0; st < S; ++st)
 #pragma unroll
-    for (int o = 0; o < NOUT; ++o) Yp[tid * SN + st * NOUT + o] = y[st][o];
+    for (int o = 0; o < NOUT; ++o) Yp[tid * C::YPS + st * NOUT + o] = y[st][o];
   __syncthreads();
   const long long p0 = tile * PPT, rem = a.n - p0;
   double lacc0 = 0.0, lacc1 = 0.0;
@@ -1465,7 +1471,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
     float* yb = Ybs + pt * SN;
     for (int i = 0; i < SN; ++i) {
       float v = 0.f;
-      for (int h = 0; h < TPPH; ++h) v += Yp[(HU ? 4 * (pt + PPT * (h >> 2)) + (h & 3) : C::item_of(pt, h)) * SN + i];
+      for (int h = 0; h < TPPH; ++h) v += Yp[(HU ? 4 * (pt + PPT * (h >> 2)) + (h & 3) : C::item_of(pt, h)) * C::YPS + i];
       yv[i] = (i < NOUT) ? v + kp[pl.off_b(L) + i] : v;
       yb[i] = 0.f;
     }
@@ -1591,13 +1597,13 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
           bb[st] = v;
         }
         tc_act_bwd1<C, ACT>(zz, bb, sa);
-        float* rd = red + ((pt * 4 + kq) * 4 + j) * NOUT;
+        float* rd = red + (kq * 4 + j) * NOUT * C::RSP + pt;
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) {
           float v = 0.f;
 #pragma unroll
           for (int st = 0; st < S; ++st) v = fmaf(sa[st], yb[st * NOUT + o], v);
-          rd[o] = v;
+          rd[o * C::RSP] = v;
         }
         slab_store1x<C, QS>(slab, pt, kq, j, bb, pt & 7);  // Zbar_{L-1} in place of Z_{L-1}
       }
@@ -1645,7 +1651,7 @@ __global__ void __launch_bounds__(128) tcw_head_kernel(WArgs a) {
       const int kq = e / (4 * NOUT), j = (e / NOUT) % 4, o = e % NOUT;
       float acc = 0.f;
       for (int pt = 0; pt < PPT; ++pt)
-        acc += HU ? red[((pt * 4 + kq) * 4 + j) * NOUT + o] : red[(j * NOUT + o) * C::HRS + C::item_of(pt, kq)];
+        acc += HU ? red[((kq * 4 + j) * NOUT + o) * C::RSP + pt] : red[(j * NOUT + o) * C::HRS + C::item_of(pt, kq)];
       pL[size_t(16 * c + 4 * kq + j) * NOUT + o] = acc;
     }
     __syncthreads();
