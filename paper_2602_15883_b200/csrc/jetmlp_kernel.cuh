@@ -260,8 +260,12 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 #ifndef FR_DW_UNROLL
 #define FR_DW_UNROLL 4
 #endif
+#ifndef FR_DW_UNROLL_TC
+#define FR_DW_UNROLL_TC 2  // split-TF32 kernel: 4.28 -> 4.16 ms at config C (unroll 1: 4.34, 3: 4.31, 4: 4.28, 8: 4.20)
+#endif
 constexpr int kGemmUnroll = FR_GEMM_UNROLL;
 constexpr int kDwUnroll = FR_DW_UNROLL;
+constexpr int kDwUnrollTC = FR_DW_UNROLL_TC;
 
 // ---------------------------------------------------------------------------
 // packed FP32 pairs (sm_100a FFMA2: fma.rn.f32x2, one issue slot for two FMAs).
@@ -1446,7 +1450,8 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
               for (int x = 0; x < 8; ++x)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc2[x][q] = 0ull;
-#pragma unroll kDwUnroll
+              constexpr int kDwU = TC ? kDwUnrollTC : kDwUnroll;
+#pragma unroll kDwU
               for (int r = 0; r < RROWS; ++r) {
                 float h[8];
                 f32x2 z[4];
