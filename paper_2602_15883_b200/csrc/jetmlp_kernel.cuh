@@ -116,12 +116,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------------------
 // compile-time configuration
 // ---------------------------------------------------------------------------
+#ifndef FR_VALUE_RPT
+#define FR_VALUE_RPT 2  // ghost producer at P = 8 (~6k points): 33 -> 20 us (1: 18 us; 6: the MSE heads)
+#endif
 template <typename T, int ACT, int MODE, int REG, int W, int NT_ = 0>
 struct JetCfg {
   using R = Regime<REG>;
   using St = Streams<MODE, REG>;
   static constexpr int DIN = R::DIN, NOUT = R::NOUT, NVEL = R::NVEL, HAS_T = R::HAS_T;
-  static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0, RPT = St::RPT;
+  static constexpr int S = St::S, NG = St::NG, NL = St::NL, LAP0 = St::LAP0;
+  // value-only rows per thread: 6 for the MSE heads; VALUE (the per-epoch ghost
+  // producer on a few thousand points) FR_VALUE_RPT, smaller tiles over more SMs
+  static constexpr int RPT = MODE == MODE_VALUE ? FR_VALUE_RPT : St::RPT;
   static constexpr bool JET = St::JET;
   static constexpr bool BWD = (MODE == MODE_PDE || MODE == MODE_MSE || MODE == MODE_GJ);
   // 12 warps per SM where the FP32 tile buffers still fit (W = 64, <= 6 streams);
@@ -260,6 +266,7 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 #ifndef FR_DW_UNROLL
 #define FR_DW_UNROLL 4
 #endif
+
 #ifndef FR_DW_UNROLL_TC
 #define FR_DW_UNROLL_TC 2  // split-TF32 kernel: 4.28 -> 4.16 ms at config C (unroll 1: 4.34, 3: 4.31, 4: 4.28, 8: 4.20)
 #endif
