@@ -153,3 +153,19 @@ def test_tc_adjoint_32_unit_steps_bit_identical_to_16():
         res[mode] = r.stdout.split()
     assert len(res["8"]) == 3
     assert res["8"] == res["4"]
+
+
+@pytest.mark.parametrize("width,tcw,wpad", [(72, 80, 128), (150, 160, 192), (200, 208, 256), (256, 256, 256),
+                                            (300, 320, 320)])
+def test_tc_tensor_width(width, tcw, wpad):
+    """TF32 plans run on their own tensor width (hidden width rounded to the
+    16-deep K chunk, to 32 above 256 units) while the parameter layout keeps
+    its 64-unit padding; FP64 and W <= 64 plans have none."""
+    from paper_2602_15883_b200 import engine
+    from paper_2602_15883_b200.network import ExpertConfig
+
+    cfg = ExpertConfig(3, 3, width, "sin", 3)
+    info = engine.get_plan(cfg, "unsteady2d", 100.0, "float32", math="tf32").info
+    assert (info.tc_width, info.width_pad) == (tcw, wpad)
+    assert engine.get_plan(cfg, "unsteady2d", 100.0, "float64").info.tc_width == 0
+    assert engine.get_plan(ExpertConfig(3, 3, 64, "tanh", 3), "unsteady2d", 100.0, "float32").info.tc_width == 0
