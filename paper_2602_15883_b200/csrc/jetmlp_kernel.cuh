@@ -833,6 +833,16 @@ __device__ __forceinline__ void run_tiles(const KArgs& a, unsigned char* smem_ra
   constexpr int NST0 = C::NST0, NSTH = C::NSTH, PP = C::PP;
   constexpr bool JET = C::JET, BWD = C::BWD;
 
+  // no tile of this dataset for this CTA (the epoch kernel's later MSE sets
+  // on most CTAs): skip the weight staging and prologue, write zero loss sums
+  if (!zero_partials && t0 >= (a.n + PPT - 1) / PPT) {
+    if constexpr (BWD)
+      if (threadIdx.x == 0 && lpart_row) {
+        lpart_row[0] = 0.0;
+        lpart_row[1] = 0.0;
+      }
+    return;
+  }
   const int L = a.L;
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* Xs = sm;                      sm += C::al(C::XELEMS);
